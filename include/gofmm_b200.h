@@ -1,0 +1,153 @@
+/* gofmm_b200.h — C-ABI of the B200-native GOFMM evaluation phase (u = K~ W).
+ *
+ * Drop-in boundary for the reference hot path
+ *     Potentials gfmm::evaluate(const HMatrix& h, const Matrix& w, const EvalOptions& opts)
+ *         /root/reference/proj/include/gfmm/evaluate.hpp:287-317
+ * The reference has no C ABI; these entry points are what a C/ctypes/cgo binding
+ * of that function would bind. Plain pointers and sizes only; no torch or Eigen types.
+ *
+ * Semantics that follow the reference exactly:
+ *   - w is N x r in ORIGINAL index order (column-major, ldw >= N);      evaluate.hpp:285-295
+ *   - u is returned N x r in PERMUTED (tree) order (column-major);       evaluate.hpp:16,312-313
+ *   - stats.flops is the reference's own flop counter formula;          evaluate.hpp:154-214
+ *   - r < 1 or a wrong row count fails with GOFMM_ERR_INVALID (the reference throws
+ *     std::invalid_argument, which its CLI maps to exit code 2);        evaluate.hpp:288-289,
+ *                                                                        gfmm_cli.cpp:289-305
+ *   - accumulation order per output block follows the reference task bodies: partners in
+ *     ascending node id (evaluate.hpp:68-70,165-174), D then near blocks in ascending block index
+ *     then proj^T c (evaluate.hpp:196-215), downward = cfar + parent term (evaluate.hpp:178-193).
+ *
+ * The compressed structure is the reference HMatrix (compress.hpp:65-79) flattened: node table
+ * (tree.hpp:13-46), skeletons (compress.hpp:39-47), near/far block lists. Arrays are copied at
+ * gofmm_create; the caller keeps ownership of everything it passes in.
+ */
+#ifndef GOFMM_B200_H
+#define GOFMM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes: mirror the reference's exception -> CLI exit code map (gfmm_cli.cpp:289-305). */
+#define GOFMM_OK 0
+#define GOFMM_ERR_INVALID 2 /* std::invalid_argument */
+#define GOFMM_ERR_IO 3      /* gfmm::io_error */
+#define GOFMM_ERR_NUMERIC 4 /* gfmm::numeric_error */
+#define GOFMM_ERR_CUDA 5    /* device failure / no device (no reference counterpart) */
+
+/* Entry sources. Kernel ids match the reference generators (oracle.hpp:141-256) plus the
+ * Exponential (Matern-1/2) kernel BASELINE config 4 needs. */
+#define GOFMM_SOURCE_STORED 0 /* D / near / far blocks supplied (DenseOracle-backed trees) */
+#define GOFMM_SOURCE_KERNEL 1 /* entries generated on device from point coordinates */
+
+#define GOFMM_KERNEL_GAUSSIAN 0    /* exp(-|xi-xj|^2 * (1/(2h^2)))      oracle.hpp:148-159, kparam[0]=h */
+#define GOFMM_KERNEL_LAPLACE 1     /* max(|xi-xj|,delta)^-(d-2)         oracle.hpp:178-192, kparam[0]=delta */
+#define GOFMM_KERNEL_POLYNOMIAL 2  /* (xi.xj + c)^p                     oracle.hpp:208-218, kparam={c,p} */
+#define GOFMM_KERNEL_EXPONENTIAL 4 /* exp(-|xi-xj| * (1/h))             Matern-1/2, kparam[0]=h */
+
+/* Block materialisation modes (GOFMM_SOURCE_KERNEL only). */
+#define GOFMM_BLOCKS_MATRIX_FREE 0 /* regenerate K entries inside the tile GEMM (never stored) */
+#define GOFMM_BLOCKS_MATERIALIZE 1 /* generate once on device at create, keep in HBM */
+
+typedef struct gofmm_tree_desc {
+  int32_t n;         /* matrix size N (HMatrix::n) */
+  int32_t num_nodes; /* nodes in BFS order, id == index, root 0 (tree.hpp:33,213-217) */
+  const int32_t* parent; /* [num_nodes] -1 for the root */
+  const int32_t* left;   /* [num_nodes] -1 at leaves; right == left + 1 */
+  const int32_t* right;  /* [num_nodes] */
+  const int32_t* level;  /* [num_nodes] root 0 */
+  const int32_t* start;  /* [num_nodes] [start,end) in permuted order */
+  const int32_t* end;    /* [num_nodes] */
+  const int32_t* iperm;  /* [n] iperm[new] = old (tree.hpp:34) */
+
+  /* skeletons (compress.hpp:39-47) */
+  const int32_t* rank;        /* [num_nodes] skeleton rank, -1 = invalid (root) */
+  const int64_t* skel_offset; /* [num_nodes+1] into skel_idx */
+  const int32_t* skel_idx;    /* original indices in CPQR pivot order (compress.hpp:174-175) */
+  const int64_t* proj_offset; /* [num_nodes+1] into proj (doubles) */
+  const double* proj;         /* per node rank x ncand, column-major (compress.hpp:177-185);
+                                 ncand = leaf size for leaves, rank(left)+rank(right) otherwise */
+
+  /* interaction lists, each pair stored once with a < b, sorted ascending (compress.hpp:261-263) */
+  int64_t num_near;
+  const int32_t* near_a; /* leaf node ids */
+  const int32_t* near_b;
+  int64_t num_far;
+  const int32_t* far_a; /* node ids, never the root; may sit on different levels */
+  const int32_t* far_b;
+
+  /* entry source */
+  int32_t source; /* GOFMM_SOURCE_* */
+  /* GOFMM_SOURCE_KERNEL */
+  int32_t kernel;       /* GOFMM_KERNEL_* */
+  int32_t dim;          /* d */
+  const double* coords; /* d x n column-major, ORIGINAL order (PointCloud::coords, oracle.hpp:13) */
+  double kparam[4];
+  /* GOFMM_SOURCE_STORED (column-major blocks exactly as HMatrix stores them) */
+  const int64_t* diag_offset; /* [num_nodes+1]; leaf_diag[id] is n_id x n_id (compress.hpp:365-371) */
+  const double* diag_blocks;
+  const int64_t* near_offset; /* [num_near+1]; K(idx a, idx b), n_a x n_b (compress.hpp:374-380) */
+  const double* near_blocks;
+  const int64_t* far_offset; /* [num_far+1]; K(skel a, skel b), k_a x k_b (compress.hpp:416-420) */
+  const double* far_blocks;
+} gofmm_tree_desc;
+
+typedef struct gofmm_options {
+  int32_t device;     /* CUDA device ordinal */
+  int32_t near_mode;  /* GOFMM_BLOCKS_* for D and near (S) blocks; default matrix-free */
+  int32_t far_mode;   /* GOFMM_BLOCKS_* for far (coupling) blocks */
+  int32_t reserved;
+} gofmm_options;
+
+typedef struct gofmm_eval_stats {
+  int64_t flops;      /* reference flop counter (Potentials::flops) */
+  double seconds;     /* wall time of the call incl. permutation (Potentials::seconds) */
+  double ms_permute;  /* device time per phase (CUDA events) */
+  double ms_upward;   /* N2S */
+  double ms_downward; /* S2S + S2N */
+  double ms_output;   /* L2L + leaf S2N */
+  double ms_h2d;      /* gofmm_evaluate only: host->device copy of w */
+  double ms_d2h;      /* gofmm_evaluate only: device->host copy of u */
+} gofmm_eval_stats;
+
+typedef struct gofmm_handle gofmm_handle;
+
+/* Build the device-resident flattened tree. opts may be NULL (defaults). */
+int gofmm_create(const gofmm_tree_desc* desc, const gofmm_options* opts, gofmm_handle** out);
+
+/* u_perm = K~ w with HOST buffers (pinned or pageable); the drop-in for gfmm::evaluate. */
+int gofmm_evaluate(gofmm_handle* h, const double* w, int64_t ldw, int32_t r, double* u_perm,
+                   int64_t ldu, gofmm_eval_stats* stats);
+
+/* Same with DEVICE buffers on `stream` (cudaStream_t, NULL = the handle's stream). Enqueues and
+ * returns; stats->flops is filled, the phase times are filled only when stats_sync != 0. */
+int gofmm_evaluate_device(gofmm_handle* h, const double* d_w, int64_t ldw, int32_t r, double* d_u_perm,
+                          int64_t ldu, void* stream, int32_t stats_sync, gofmm_eval_stats* stats);
+
+/* unpermute (evaluate.hpp:21-25) on device: u[iperm[t], :] = u_perm[t, :]. */
+int gofmm_unpermute_device(gofmm_handle* h, const double* d_u_perm, int64_t ldp, int32_t r, double* d_u,
+                           int64_t ldu, void* stream);
+
+/* Reference flop count (Potentials::flops) for r right-hand sides, without evaluating. */
+int64_t gofmm_flops(const gofmm_handle* h, int32_t r);
+
+/* Bytes of device memory held by the handle (tree + workspace). */
+int64_t gofmm_device_bytes(const gofmm_handle* h);
+
+/* Number of kernel launches one evaluation issues (for the bench's gpu_launches). */
+int32_t gofmm_launches_per_eval(const gofmm_handle* h);
+
+int gofmm_destroy(gofmm_handle* h);
+
+/* Message of the last failure on the calling thread ("" if none). */
+const char* gofmm_last_error(void);
+
+int32_t gofmm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GOFMM_B200_H */

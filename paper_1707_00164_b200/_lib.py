@@ -1,0 +1,130 @@
+"""Loader for the in-tree sm_100a extension ``_lib/libgofmm_b200.so`` (C-ABI of include/gofmm_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is present, every entry
+point fails loudly (GofmmError with GOFMM_ERR_CUDA), mirroring north_star's "no CPU fallback".
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import sys
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+REPO_DIR = os.path.dirname(PKG_DIR)
+LIB_PATH = os.path.join(PKG_DIR, "_lib", "libgofmm_b200.so")
+CSRC = os.path.join(PKG_DIR, "csrc")
+INCLUDE = os.path.join(REPO_DIR, "include")
+
+GOFMM_OK = 0
+GOFMM_ERR_INVALID = 2
+GOFMM_ERR_IO = 3
+GOFMM_ERR_NUMERIC = 4
+GOFMM_ERR_CUDA = 5
+
+SOURCE_STORED = 0
+SOURCE_KERNEL = 1
+KERNEL_GAUSSIAN = 0
+KERNEL_LAPLACE = 1
+KERNEL_POLYNOMIAL = 2
+KERNEL_EXPONENTIAL = 4
+BLOCKS_MATRIX_FREE = 0
+BLOCKS_MATERIALIZE = 1
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared"]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile the CUDA extension in-tree with nvcc for sm_100a (cross-compiles without a GPU)."""
+    srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cu", ".cuh", ".h"))]
+    srcs.append(os.path.join(INCLUDE, "gofmm_b200.h"))
+    if not force and os.path.exists(LIB_PATH):
+        newest = max(os.path.getmtime(s) for s in srcs)
+        if os.path.getmtime(LIB_PATH) >= newest:
+            return LIB_PATH
+    os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, os.path.join(CSRC, "gofmm_capi.cu")]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+class TreeDesc(C.Structure):
+    _fields_ = [
+        ("n", C.c_int32), ("num_nodes", C.c_int32),
+        ("parent", C.c_void_p), ("left", C.c_void_p), ("right", C.c_void_p), ("level", C.c_void_p),
+        ("start", C.c_void_p), ("end", C.c_void_p), ("iperm", C.c_void_p),
+        ("rank", C.c_void_p), ("skel_offset", C.c_void_p), ("skel_idx", C.c_void_p),
+        ("proj_offset", C.c_void_p), ("proj", C.c_void_p),
+        ("num_near", C.c_int64), ("near_a", C.c_void_p), ("near_b", C.c_void_p),
+        ("num_far", C.c_int64), ("far_a", C.c_void_p), ("far_b", C.c_void_p),
+        ("source", C.c_int32), ("kernel", C.c_int32), ("dim", C.c_int32), ("coords", C.c_void_p),
+        ("kparam", C.c_double * 4),
+        ("diag_offset", C.c_void_p), ("diag_blocks", C.c_void_p),
+        ("near_offset", C.c_void_p), ("near_blocks", C.c_void_p),
+        ("far_offset", C.c_void_p), ("far_blocks", C.c_void_p),
+    ]
+
+
+class Options(C.Structure):
+    _fields_ = [("device", C.c_int32), ("near_mode", C.c_int32), ("far_mode", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class EvalStats(C.Structure):
+    _fields_ = [("flops", C.c_int64), ("seconds", C.c_double), ("ms_permute", C.c_double),
+                ("ms_upward", C.c_double), ("ms_downward", C.c_double), ("ms_output", C.c_double),
+                ("ms_h2d", C.c_double), ("ms_d2h", C.c_double)]
+
+
+class GofmmError(RuntimeError):
+    """Raised for non-zero C-ABI return codes; ``code`` follows gfmm_cli.cpp:289-305."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class InvalidArgument(GofmmError, ValueError):
+    """std::invalid_argument in the reference (evaluate.hpp:288-289)."""
+
+
+_lib = None
+
+# every symbol include/gofmm_b200.h declares
+EXPORTS = ("gofmm_create", "gofmm_evaluate", "gofmm_evaluate_device", "gofmm_unpermute_device",
+           "gofmm_flops", "gofmm_device_bytes", "gofmm_launches_per_eval", "gofmm_destroy",
+           "gofmm_last_error", "gofmm_abi_version")
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise GofmmError(GOFMM_ERR_CUDA, f"CUDA extension not built: {LIB_PATH} (run __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        L.gofmm_create.argtypes = [C.POINTER(TreeDesc), C.POINTER(Options), C.POINTER(P)]
+        L.gofmm_evaluate.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, C.POINTER(EvalStats)]
+        L.gofmm_evaluate_device.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, P, C.c_int32,
+                                            C.POINTER(EvalStats)]
+        L.gofmm_unpermute_device.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, P]
+        L.gofmm_flops.argtypes = [P, C.c_int32]
+        L.gofmm_flops.restype = C.c_int64
+        L.gofmm_device_bytes.argtypes = [P]
+        L.gofmm_device_bytes.restype = C.c_int64
+        L.gofmm_launches_per_eval.argtypes = [P]
+        L.gofmm_destroy.argtypes = [P]
+        L.gofmm_last_error.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def check(rc: int):
+    if rc != GOFMM_OK:
+        msg = lib().gofmm_last_error().decode()
+        if rc == GOFMM_ERR_INVALID:
+            raise InvalidArgument(rc, msg)
+        raise GofmmError(rc, msg)

@@ -1,0 +1,942 @@
+// gofmm_capi.cu — host side of the B200-native GOFMM evaluation phase behind include/gofmm_b200.h.
+//
+// Replaces the reference executor (evaluate.hpp:52-120 traversal_schedule, :222-281
+// execute_levels / execute_dag, common.hpp:109-126 parallel_for) with a plan built ONCE at
+// gofmm_create over a device-resident flattened tree, executed as level-synchronous launches
+// on one stream:
+//     permute W (K5)  ->  N2S levels depth..1  ->  DOWNWARD levels 1..depth  ->  OUTPUT
+// Each launch is the grouped multi-term FP64 DMMA GEMM of gofmm_kernels.cuh.
+//
+// HBM layout (all FP64, column-major, every block start 16-byte aligned for cp.async):
+//   point space    : leaves left-to-right, leaf a at rows [pst_a, pst_a + pad2(n_a)); W_perm and
+//                    the permuted coordinates live here (padding rows are zero)
+//   skeleton space : nodes in BFS id order (== level order), node a at rows
+//                    [soff_a, soff_a + pad2(k_a)); what (N2S output) and c (downward) live here.
+//                    Siblings are adjacent, so [what_l; what_r] is one contiguous row range.
+//   proj_a         : k_a x ncand_pad column-major, ld = pad2(k_a); interior proj gets a zero
+//                    column after each odd-rank child so its columns line up with skeleton space.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gofmm_b200.h"
+#include "gofmm_kernels.cuh"
+
+namespace gofmm {
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define GOFMM_CUDA(x)                                                                        \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess)                                                                   \
+      throw Error(GOFMM_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));         \
+  } while (0)
+
+inline int64_t pad2(int64_t x) { return (x + 1) & ~int64_t(1); }
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void alloc(size_t b, bool zero = true) {
+    release();
+    if (b == 0) return;
+    GOFMM_CUDA(cudaMalloc(&p, b));
+    bytes = b;
+    if (zero) GOFMM_CUDA(cudaMemset(p, 0, b));
+  }
+  template <class T>
+  void upload(const std::vector<T>& v) {
+    alloc(v.size() * sizeof(T), false);
+    if (!v.empty()) GOFMM_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// ---------------------------------------------------------------- kernel configurations
+// S: stored-operand GEMMs (N2S / downward / output without generation).
+// G: generated-operand GEMMs (matrix-free L2L and S2S): warps split M only, so every A entry is
+//    generated exactly once per CTA, and BN is wide to amortise exp() over the RHS columns.
+constexpr int kBK = 16, kStages = 3, kBM_S = 128, kBM_G = 64;
+#define CFG_S kBM_S, 128, 4, 2, kBK, kStages
+#define CFG_G kBM_G, 256, 8, 1, kBK, kStages
+using ShapeS = GemmShape<CFG_S>;
+using ShapeG = GemmShape<CFG_G>;
+
+using KernelFn = void (*)(const Tile*, const Group*, const Term*, int32_t, KernelParams, double*, int64_t);
+
+template <int KIND, int DIM>
+KernelFn gen_kernel() {
+  return &grouped_gemm_f64<CFG_G, KIND, DIM>;
+}
+
+KernelFn pick_gen_kernel(int kind, int dim) {
+#define GOFMM_DIMS(K)                        \
+  switch (dim) {                             \
+    case 1: return gen_kernel<K, 1>();       \
+    case 2: return gen_kernel<K, 2>();       \
+    case 3: return gen_kernel<K, 3>();       \
+    case 4: return gen_kernel<K, 4>();       \
+    case 6: return gen_kernel<K, 6>();       \
+    case 8: return gen_kernel<K, 8>();       \
+    default: return gen_kernel<K, 0>();      \
+  }
+  switch (kind) {
+    case kGaussian: GOFMM_DIMS(kGaussian)
+    case kLaplace: GOFMM_DIMS(kLaplace)
+    case kPolynomial: GOFMM_DIMS(kPolynomial)
+    case kExponential: GOFMM_DIMS(kExponential)
+  }
+#undef GOFMM_DIMS
+  throw Error(GOFMM_ERR_INVALID, "unsupported kernel id " + std::to_string(kind));
+}
+
+template <int KIND, int DIM>
+void launch_generate(const double* xr, int rows, const double* xc, int cols, double* out, int64_t ld,
+                     const KernelParams& kp, cudaStream_t st) {
+  dim3 grid((rows + 127) / 128, cols);
+  generate_block<KIND, DIM><<<grid, 128, 0, st>>>(xr, rows, xc, cols, out, ld, kp);
+}
+
+void generate_dispatch(int kind, int dim, const double* xr, int rows, const double* xc, int cols, double* out,
+                       int64_t ld, const KernelParams& kp, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+#define GOFMM_GEN(K)                                                      \
+  switch (dim) {                                                          \
+    case 3: launch_generate<K, 3>(xr, rows, xc, cols, out, ld, kp, st); return; \
+    case 8: launch_generate<K, 8>(xr, rows, xc, cols, out, ld, kp, st); return; \
+    default: launch_generate<K, 0>(xr, rows, xc, cols, out, ld, kp, st); return; \
+  }
+  switch (kind) {
+    case kGaussian: GOFMM_GEN(kGaussian)
+    case kLaplace: GOFMM_GEN(kLaplace)
+    case kPolynomial: GOFMM_GEN(kPolynomial)
+    case kExponential: GOFMM_GEN(kExponential)
+  }
+#undef GOFMM_GEN
+  throw Error(GOFMM_ERR_INVALID, "unsupported kernel id " + std::to_string(kind));
+}
+
+// ---------------------------------------------------------------- plan
+enum class Buf { Wp, What, C, Out };  // B operand / output bases (resolved per workspace)
+
+struct HostTerm {
+  int kind;         // 0 stored A, 1 generated
+  bool row_major;   // stored A is accessed transposed
+  int64_t a_off;    // offset (doubles) into the A blob (blob id below)
+  int a_blob;       // 0 proj, 1 diag, 2 near, 3 far
+  int64_t lda;
+  Buf b_buf;
+  int64_t b_row;    // row offset within the B buffer
+  int K;
+  int64_t xr_off, xc_off;  // generated: point offsets (in points) into coordinate blob
+  int x_blob;              // 0 point space (Xp), 1 skeleton space (Xs)
+};
+
+struct HostGroup {
+  int64_t c_row;
+  int M;
+  std::vector<HostTerm> terms;
+};
+
+struct Launch {
+  int first_tile = 0, ntiles = 0;
+  bool gen = false;  // G config (generated operands present)
+  Buf out;
+  int phase;  // 0 upward, 1 downward, 2 output
+};
+
+}  // namespace
+}  // namespace gofmm
+
+struct gofmm_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[8] = {};
+  int32_t n = 0, num_nodes = 0, depth = 0, dim = 0, kernel = -1, source = 0;
+  gofmm::KernelParams kp{};
+  int near_mode = GOFMM_BLOCKS_MATRIX_FREE, far_mode = GOFMM_BLOCKS_MATRIX_FREE;
+
+  // host copies of the structure
+  std::vector<int32_t> parent, left, right, level, start, end, iperm, rank;
+  std::vector<int32_t> leaf_ids;
+  std::vector<int64_t> pst, soff;  // point / skeleton space offsets per node (-1 if none)
+  int64_t ld_wp = 0, ld_s = 0;
+  std::vector<int32_t> near_a, near_b, far_a, far_b;
+
+  // device tree
+  gofmm::DevBuf d_proj, d_diag, d_near, d_far, d_xp, d_xs, d_prow, d_iperm;
+  std::vector<int64_t> proj_off, diag_off, near_off, far_off;  // device blob offsets (doubles)
+
+  // plan
+  std::vector<gofmm::HostGroup> groups;
+  std::vector<gofmm::Launch> launches;
+  std::vector<gofmm::Tile> tiles;
+  gofmm::DevBuf d_tiles, d_groups, d_terms;
+  bool plan_uploaded = false;
+  int32_t plan_r = 0;  // workspace r the device term pointers were built for
+
+  // workspace
+  gofmm::DevBuf d_wp, d_what, d_c, d_win, d_uout;
+  int32_t ws_r = 0;
+
+  gofmm::KernelFn kfn_s = nullptr, kfn_g = nullptr;
+  int64_t flops_per_rhs = 0;
+};
+
+namespace gofmm {
+namespace {
+
+void validate(const gofmm_tree_desc* d) {
+  if (!d) throw Error(GOFMM_ERR_INVALID, "null descriptor");
+  if (d->n < 1) throw Error(GOFMM_ERR_INVALID, "n must be >= 1");
+  if (d->num_nodes < 1) throw Error(GOFMM_ERR_INVALID, "num_nodes must be >= 1");
+  if (!d->parent || !d->left || !d->right || !d->level || !d->start || !d->end || !d->iperm || !d->rank)
+    throw Error(GOFMM_ERR_INVALID, "missing node arrays");
+  const int nn = d->num_nodes;
+  for (int i = 0; i < nn; ++i) {
+    if (d->start[i] < 0 || d->end[i] > d->n || d->start[i] > d->end[i])
+      throw Error(GOFMM_ERR_INVALID, "node range out of bounds");
+    if (d->left[i] >= 0) {
+      if (d->left[i] >= nn || d->right[i] != d->left[i] + 1 || d->right[i] >= nn)
+        throw Error(GOFMM_ERR_INVALID, "children must be consecutive ids (tree.hpp:213-217)");
+      if (d->left[i] <= i) throw Error(GOFMM_ERR_INVALID, "nodes must be in BFS order");
+    }
+    if (i > 0 && (d->level[i] < d->level[i - 1]))
+      throw Error(GOFMM_ERR_INVALID, "nodes must be in level (BFS) order");
+  }
+  if (d->parent[0] != -1 || d->start[0] != 0 || d->end[0] != d->n)
+    throw Error(GOFMM_ERR_INVALID, "node 0 must be the root covering [0, n)");
+  if (d->num_near < 0 || d->num_far < 0) throw Error(GOFMM_ERR_INVALID, "negative list size");
+  if (d->source != GOFMM_SOURCE_STORED && d->source != GOFMM_SOURCE_KERNEL)
+    throw Error(GOFMM_ERR_INVALID, "unknown entry source");
+  if (d->source == GOFMM_SOURCE_KERNEL && (!d->coords || d->dim < 1 || d->dim > kMaxDimRt))
+    throw Error(GOFMM_ERR_INVALID, "kernel source needs coords and 1 <= dim <= 16");
+  if (d->source == GOFMM_SOURCE_STORED && (!d->diag_offset || !d->diag_blocks))
+    throw Error(GOFMM_ERR_INVALID, "stored source needs leaf_diag blocks");
+}
+
+void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
+  const int nn = d->num_nodes;
+  H->n = d->n;
+  H->num_nodes = nn;
+  H->source = d->source;
+  H->kernel = d->source == GOFMM_SOURCE_KERNEL ? d->kernel : -1;
+  H->dim = d->source == GOFMM_SOURCE_KERNEL ? d->dim : 0;
+  if (o) {
+    H->near_mode = o->near_mode;
+    H->far_mode = o->far_mode;
+  }
+  auto cp = [&](std::vector<int32_t>& v, const int32_t* p, int64_t k) { v.assign(p, p + k); };
+  cp(H->parent, d->parent, nn);
+  cp(H->left, d->left, nn);
+  cp(H->right, d->right, nn);
+  cp(H->level, d->level, nn);
+  cp(H->start, d->start, nn);
+  cp(H->end, d->end, nn);
+  cp(H->iperm, d->iperm, d->n);
+  cp(H->rank, d->rank, nn);
+  cp(H->near_a, d->near_a, d->num_near);
+  cp(H->near_b, d->near_b, d->num_near);
+  cp(H->far_a, d->far_a, d->num_far);
+  cp(H->far_b, d->far_b, d->num_far);
+  H->depth = 0;
+  for (int i = 0; i < nn; ++i) H->depth = std::max(H->depth, H->level[i]);
+
+  // kernel parameters exactly as the reference oracles precompute them
+  if (H->kernel == kGaussian) {
+    double h = d->kparam[0];
+    if (!(h > 0)) throw Error(GOFMM_ERR_INVALID, "gaussian bandwidth must be positive");
+    H->kp.p0 = 1.0 / (2.0 * h * h);  // oracle.hpp:151
+  } else if (H->kernel == kExponential) {
+    if (!(d->kparam[0] > 0)) throw Error(GOFMM_ERR_INVALID, "exponential bandwidth must be positive");
+    H->kp.p0 = 1.0 / d->kparam[0];
+  } else if (H->kernel == kLaplace) {
+    if (d->kparam[0] < 0) throw Error(GOFMM_ERR_INVALID, "laplace regularization must be >= 0");
+    H->kp.p0 = d->kparam[0];
+    H->kp.p1 = double(d->dim - 2);  // oracle.hpp:181
+  } else if (H->kernel == kPolynomial) {
+    H->kp.p0 = d->kparam[0];
+    H->kp.p1 = double(static_cast<int>(d->kparam[1]));
+  } else if (d->source == GOFMM_SOURCE_KERNEL) {
+    throw Error(GOFMM_ERR_INVALID, "unsupported kernel id");
+  }
+  H->kp.dim = H->dim;
+
+  // skeleton validity & consistency
+  std::vector<int32_t> ncand(nn, 0);
+  for (int i = 0; i < nn; ++i) {
+    const int k = H->rank[i];
+    if (k < 0) continue;
+    int64_t np = d->proj_offset[i + 1] - d->proj_offset[i];
+    const bool leaf = H->left[i] < 0;
+    int64_t c = leaf ? (H->end[i] - H->start[i]) : 0;
+    if (!leaf) {
+      if (H->rank[H->left[i]] < 0 || H->rank[H->right[i]] < 0)
+        throw Error(GOFMM_ERR_INVALID, "interior skeleton needs valid child skeletons");
+      c = H->rank[H->left[i]] + H->rank[H->right[i]];
+    }
+    if (np != int64_t(k) * c) throw Error(GOFMM_ERR_INVALID, "proj size mismatch at node " + std::to_string(i));
+    if (d->skel_offset[i + 1] - d->skel_offset[i] != k)
+      throw Error(GOFMM_ERR_INVALID, "skeleton index count mismatch at node " + std::to_string(i));
+    ncand[i] = static_cast<int32_t>(c);
+  }
+
+  // leaves left-to-right (tree.hpp:232-233) and point space
+  for (int i = 0; i < nn; ++i)
+    if (H->left[i] < 0) H->leaf_ids.push_back(i);
+  std::sort(H->leaf_ids.begin(), H->leaf_ids.end(), [&](int a, int b) { return H->start[a] < H->start[b]; });
+  H->pst.assign(nn, -1);
+  int64_t off = 0;
+  for (int id : H->leaf_ids) {
+    H->pst[id] = off;
+    off += pad2(H->end[id] - H->start[id]);
+  }
+  H->ld_wp = std::max<int64_t>(pad2(off), 2);
+  // skeleton space (BFS id order)
+  H->soff.assign(nn, -1);
+  off = 0;
+  for (int i = 0; i < nn; ++i) {
+    if (H->rank[i] < 0) continue;
+    H->soff[i] = off;
+    off += pad2(H->rank[i]);
+  }
+  H->ld_s = std::max<int64_t>(pad2(off), 2);
+
+  // row map for the permutation kernel, and iperm
+  std::vector<int32_t> prow(H->ld_wp, -1);
+  for (int id : H->leaf_ids)
+    for (int t = H->start[id]; t < H->end[id]; ++t) prow[H->pst[id] + (t - H->start[id])] = H->iperm[t];
+  H->d_prow.upload(prow);
+  H->d_iperm.upload(H->iperm);
+
+  // padded proj blob
+  {
+    std::vector<double> blob;
+    H->proj_off.assign(nn, -1);
+    for (int i = 0; i < nn; ++i) {
+      const int k = H->rank[i];
+      if (k < 0) continue;
+      const int64_t ld = pad2(k);
+      const double* src = d->proj + d->proj_offset[i];
+      H->proj_off[i] = static_cast<int64_t>(blob.size());
+      if (H->left[i] < 0) {
+        const int c = ncand[i];
+        blob.resize(blob.size() + ld * c, 0.0);
+        double* dst = blob.data() + H->proj_off[i];
+        for (int j = 0; j < c; ++j)
+          for (int r = 0; r < k; ++r) dst[r + j * ld] = src[r + int64_t(j) * k];
+      } else {
+        const int kl = H->rank[H->left[i]], kr = H->rank[H->right[i]];
+        const int64_t cpad = pad2(kl) + pad2(kr);
+        blob.resize(blob.size() + ld * cpad, 0.0);
+        double* dst = blob.data() + H->proj_off[i];
+        for (int j = 0; j < kl + kr; ++j) {
+          const int64_t jj = (j < kl) ? j : pad2(kl) + (j - kl);
+          for (int r = 0; r < k; ++r) dst[r + jj * ld] = src[r + int64_t(j) * k];
+        }
+      }
+      while (blob.size() % 2) blob.push_back(0.0);
+    }
+    H->d_proj.upload(blob);
+  }
+
+  // coordinates: permuted point space and skeleton space, point-major
+  if (d->source == GOFMM_SOURCE_KERNEL) {
+    const int D = d->dim;
+    std::vector<double> xp(size_t(H->ld_wp) * D, 0.0);
+    for (int id : H->leaf_ids)
+      for (int t = H->start[id]; t < H->end[id]; ++t) {
+        const int64_t row = H->pst[id] + (t - H->start[id]);
+        const double* src = d->coords + int64_t(H->iperm[t]) * D;
+        for (int q = 0; q < D; ++q) xp[row * D + q] = src[q];
+      }
+    H->d_xp.upload(xp);
+    std::vector<double> xs(size_t(H->ld_s) * D, 0.0);
+    for (int i = 0; i < nn; ++i) {
+      if (H->rank[i] < 0) continue;
+      for (int l = 0; l < H->rank[i]; ++l) {
+        const int64_t orig = d->skel_idx[d->skel_offset[i] + l];
+        if (orig < 0 || orig >= d->n) throw Error(GOFMM_ERR_INVALID, "skeleton index out of range");
+        for (int q = 0; q < D; ++q) xs[(H->soff[i] + l) * D + q] = d->coords[orig * D + q];
+      }
+    }
+    H->d_xs.upload(xs);
+  }
+
+  // stored / materialised blocks: D (leaf_diag), near, far — column-major, ld = pad2(rows)
+  const bool stored = d->source == GOFMM_SOURCE_STORED;
+  const bool mat_near = !stored && H->near_mode == GOFMM_BLOCKS_MATERIALIZE;
+  const bool mat_far = !stored && H->far_mode == GOFMM_BLOCKS_MATERIALIZE;
+  auto nrows = [&](int id) { return H->end[id] - H->start[id]; };
+  auto pack_blocks = [&](int64_t count, auto rows_of, auto cols_of, const int64_t* src_off, const double* src,
+                         std::vector<int64_t>& offs, DevBuf& dev, bool from_host) {
+    offs.assign(count, -1);
+    int64_t total = 0;
+    for (int64_t t = 0; t < count; ++t) {
+      int r = rows_of(t), c = cols_of(t);
+      if (r <= 0 || c <= 0) continue;
+      offs[t] = total;
+      total += pad2(r) * c;
+    }
+    if (!from_host) {
+      dev.alloc(std::max<int64_t>(total, 2) * sizeof(double));
+      return;
+    }
+    std::vector<double> blob(std::max<int64_t>(total, 2), 0.0);
+    for (int64_t t = 0; t < count; ++t) {
+      if (offs[t] < 0) continue;
+      int r = rows_of(t), c = cols_of(t);
+      if (src_off[t + 1] - src_off[t] != int64_t(r) * c)
+        throw Error(GOFMM_ERR_INVALID, "stored block size mismatch");
+      const double* s = src + src_off[t];
+      double* dd = blob.data() + offs[t];
+      const int64_t ld = pad2(r);
+      for (int j = 0; j < c; ++j)
+        for (int i = 0; i < r; ++i) dd[i + j * ld] = s[i + int64_t(j) * r];
+    }
+    dev.upload(blob);
+  };
+  if (stored || mat_near) {
+    pack_blocks(
+        nn, [&](int64_t t) { return H->left[t] < 0 ? nrows(int(t)) : 0; },
+        [&](int64_t t) { return H->left[t] < 0 ? nrows(int(t)) : 0; }, d->diag_offset, d->diag_blocks, H->diag_off,
+        H->d_diag, stored);
+    if (stored && d->num_near && (!d->near_offset || !d->near_blocks))
+      throw Error(GOFMM_ERR_INVALID, "stored source needs near blocks");
+    pack_blocks(
+        d->num_near, [&](int64_t t) { return nrows(H->near_a[t]); }, [&](int64_t t) { return nrows(H->near_b[t]); },
+        d->near_offset, d->near_blocks, H->near_off, H->d_near, stored);
+  }
+  if (stored || mat_far) {
+    if (stored && d->num_far && (!d->far_offset || !d->far_blocks))
+      throw Error(GOFMM_ERR_INVALID, "stored source needs far blocks");
+    pack_blocks(
+        d->num_far, [&](int64_t t) { return H->rank[H->far_a[t]]; }, [&](int64_t t) { return H->rank[H->far_b[t]]; },
+        d->far_offset, d->far_blocks, H->far_off, H->d_far, stored);
+  }
+  // device-side materialisation from coordinates
+  if (mat_near) {
+    const double* xp = H->d_xp.as<double>();
+    for (int id : H->leaf_ids)
+      generate_dispatch(H->kernel, H->dim, xp + H->pst[id] * H->dim, nrows(id), xp + H->pst[id] * H->dim, nrows(id),
+                        H->d_diag.as<double>() + H->diag_off[id], pad2(nrows(id)), H->kp, H->stream);
+    for (size_t t = 0; t < H->near_a.size(); ++t) {
+      int a = H->near_a[t], b = H->near_b[t];
+      generate_dispatch(H->kernel, H->dim, xp + H->pst[a] * H->dim, nrows(a), xp + H->pst[b] * H->dim, nrows(b),
+                        H->d_near.as<double>() + H->near_off[t], pad2(nrows(a)), H->kp, H->stream);
+    }
+  }
+  if (mat_far) {
+    const double* xs = H->d_xs.as<double>();
+    for (size_t t = 0; t < H->far_a.size(); ++t) {
+      int a = H->far_a[t], b = H->far_b[t];
+      generate_dispatch(H->kernel, H->dim, xs + H->soff[a] * H->dim, H->rank[a], xs + H->soff[b] * H->dim, H->rank[b],
+                        H->d_far.as<double>() + H->far_off[t], pad2(H->rank[a]), H->kp, H->stream);
+    }
+  }
+  GOFMM_CUDA(cudaStreamSynchronize(H->stream));
+  GOFMM_CUDA(cudaGetLastError());
+
+  // ------------------------------------------------------------ groups / terms (evaluate.hpp:52-217)
+  // partners per node, ascending partner id (evaluate.hpp:63-70)
+  struct Partner {
+    int other, block;
+    bool transposed;
+  };
+  std::vector<std::vector<Partner>> partners(nn);
+  for (size_t t = 0; t < H->far_a.size(); ++t) {
+    int a = H->far_a[t], b = H->far_b[t];
+    if (a < 0 || b < 0 || a >= nn || b >= nn || H->rank[a] < 0 || H->rank[b] < 0)
+      throw Error(GOFMM_ERR_INVALID, "far pair references a node without skeleton");
+    partners[a].push_back({b, int(t), false});
+    partners[b].push_back({a, int(t), true});
+  }
+  for (auto& ps : partners)
+    std::stable_sort(ps.begin(), ps.end(), [](const Partner& x, const Partner& y) { return x.other < y.other; });
+  std::vector<std::vector<int>> near_of(nn);
+  for (size_t t = 0; t < H->near_a.size(); ++t) {
+    int a = H->near_a[t], b = H->near_b[t];
+    if (a < 0 || b < 0 || a >= nn || b >= nn || H->left[a] >= 0 || H->left[b] >= 0)
+      throw Error(GOFMM_ERR_INVALID, "near pair must join two leaves");
+    near_of[a].push_back(int(t));
+    near_of[b].push_back(int(t));
+  }
+
+  const bool gen_near = !stored && !mat_near;
+  const bool gen_far = !stored && !mat_far;
+  int64_t flops = 0;
+  auto push_launch = [&](std::vector<HostGroup>& gs, bool gen, Buf out, int phase) {
+    Launch L;
+    L.first_tile = int(H->tiles.size());
+    L.gen = gen;
+    L.out = out;
+    L.phase = phase;
+    const int BM = gen ? kBM_G : kBM_S;
+    for (auto& g : gs) {
+      const int gid = int(H->groups.size());
+      for (int m0 = 0; m0 < std::max(g.M, 0); m0 += BM) H->tiles.push_back({gid, m0});
+      H->groups.push_back(std::move(g));
+    }
+    L.ntiles = int(H->tiles.size()) - L.first_tile;
+    if (L.ntiles > 0) H->launches.push_back(L);
+  };
+
+  // upward (N2S), deepest level first (evaluate.hpp:83-93,150-163)
+  for (int lev = H->depth; lev >= 1; --lev) {
+    std::vector<HostGroup> gs;
+    for (int i = 0; i < nn; ++i) {
+      if (H->level[i] != lev || H->rank[i] < 0) continue;
+      HostGroup g;
+      g.c_row = H->soff[i];
+      g.M = H->rank[i];
+      HostTerm t{};
+      t.kind = 0;
+      t.row_major = false;
+      t.a_blob = 0;
+      t.a_off = H->proj_off[i];
+      t.lda = pad2(H->rank[i]);
+      if (H->left[i] < 0) {
+        t.b_buf = Buf::Wp;
+        t.b_row = H->pst[i];
+        t.K = nrows(i);
+      } else {
+        t.b_buf = Buf::What;
+        t.b_row = H->soff[H->left[i]];
+        t.K = int(pad2(H->rank[H->left[i]]) + pad2(H->rank[H->right[i]]));
+      }
+      flops += 2LL * H->rank[i] * ncand[i];
+      g.terms.push_back(t);
+      gs.push_back(std::move(g));
+    }
+    push_launch(gs, false, Buf::What, 0);
+  }
+
+  // downward: coupling (S2S) + parent term (S2N), top level first (evaluate.hpp:95-111,164-195)
+  for (int lev = 1; lev <= H->depth; ++lev) {
+    std::vector<HostGroup> gs;
+    bool any_gen = false;
+    for (int i = 0; i < nn; ++i) {
+      if (H->level[i] != lev || H->rank[i] < 0) continue;
+      HostGroup g;
+      g.c_row = H->soff[i];
+      g.M = H->rank[i];
+      for (const Partner& p : partners[i]) {
+        HostTerm t{};
+        t.b_buf = Buf::What;
+        t.b_row = H->soff[p.other];
+        t.K = H->rank[p.other];
+        if (gen_far) {
+          t.kind = 1;
+          t.x_blob = 1;
+          t.xr_off = H->soff[i];
+          t.xc_off = H->soff[p.other];
+          any_gen = true;
+        } else {
+          t.kind = 0;
+          t.a_blob = 3;
+          t.a_off = H->far_off[p.block];
+          t.lda = pad2(H->rank[H->far_a[p.block]]);
+          t.row_major = p.transposed;
+        }
+        flops += 2LL * H->rank[i] * H->rank[p.other];
+        g.terms.push_back(t);
+      }
+      const int par = H->parent[i];
+      if (par > 0 && H->rank[par] >= 0) {
+        HostTerm t{};
+        t.kind = 0;
+        t.row_major = true;  // proj_p[:, off:off+k]^T
+        t.a_blob = 0;
+        const int64_t coloff = (i == H->left[par]) ? 0 : pad2(H->rank[H->left[par]]);
+        t.lda = pad2(H->rank[par]);
+        t.a_off = H->proj_off[par] + coloff * t.lda;
+        t.b_buf = Buf::C;
+        t.b_row = H->soff[par];
+        t.K = H->rank[par];
+        flops += 2LL * H->rank[par] * H->rank[i];
+        g.terms.push_back(t);
+      }
+      gs.push_back(std::move(g));
+    }
+    push_launch(gs, any_gen, Buf::C, 1);
+  }
+
+  // output: D, near blocks (ascending index), proj^T c (evaluate.hpp:113-117,196-217)
+  {
+    std::vector<HostGroup> gs;
+    for (int id : H->leaf_ids) {
+      HostGroup g;
+      g.c_row = H->start[id];
+      g.M = nrows(id);
+      const int n_a = nrows(id);
+      HostTerm t{};
+      t.b_buf = Buf::Wp;
+      t.b_row = H->pst[id];
+      t.K = n_a;
+      if (gen_near) {
+        t.kind = 1;
+        t.x_blob = 0;
+        t.xr_off = H->pst[id];
+        t.xc_off = H->pst[id];
+      } else {
+        t.kind = 0;
+        t.a_blob = 1;
+        t.a_off = H->diag_off[id];
+        t.lda = pad2(n_a);
+      }
+      flops += 2LL * n_a * n_a;
+      g.terms.push_back(t);
+      for (int bi : near_of[id]) {
+        const int a = H->near_a[bi], b = H->near_b[bi];
+        const int other = (a == id) ? b : a;
+        HostTerm u{};
+        u.b_buf = Buf::Wp;
+        u.b_row = H->pst[other];
+        u.K = nrows(other);
+        if (gen_near) {
+          u.kind = 1;
+          u.x_blob = 0;
+          u.xr_off = H->pst[id];
+          u.xc_off = H->pst[other];
+        } else {
+          u.kind = 0;
+          u.a_blob = 2;
+          u.a_off = H->near_off[bi];
+          u.lda = pad2(nrows(a));
+          u.row_major = (a != id);  // K_ab^T for the b side (evaluate.hpp:205-207)
+        }
+        flops += 2LL * nrows(a) * nrows(b);
+        g.terms.push_back(u);
+      }
+      if (H->rank[id] >= 0) {
+        HostTerm v{};
+        v.kind = 0;
+        v.row_major = true;  // proj^T
+        v.a_blob = 0;
+        v.a_off = H->proj_off[id];
+        v.lda = pad2(H->rank[id]);
+        v.b_buf = Buf::C;
+        v.b_row = H->soff[id];
+        v.K = H->rank[id];
+        flops += 2LL * H->rank[id] * n_a;
+        g.terms.push_back(v);
+      }
+      gs.push_back(std::move(g));
+    }
+    push_launch(gs, gen_near, Buf::Out, 2);
+  }
+  H->flops_per_rhs = flops;
+
+  H->kfn_s = &grouped_gemm_f64<CFG_S, kKindNone, 1>;
+  size_t smem_s = ShapeS::smem_bytes(0);
+  GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_s)));
+  if (!stored && (gen_near || gen_far)) {
+    H->kfn_g = pick_gen_kernel(H->kernel, H->dim);
+    const int dmax = (H->dim == 1 || H->dim == 2 || H->dim == 3 || H->dim == 4 || H->dim == 6 || H->dim == 8)
+                         ? H->dim
+                         : kMaxDimRt;
+    size_t smem_g = ShapeG::smem_bytes(dmax);
+    GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_g, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_g)));
+  }
+  H->d_tiles.upload(H->tiles);
+  H->d_groups.alloc(H->groups.size() * sizeof(Group), false);
+  size_t nterms = 0;
+  for (auto& g : H->groups) nterms += g.terms.size();
+  H->d_terms.alloc(std::max<size_t>(nterms, 1) * sizeof(Term), false);
+}
+
+void ensure_workspace(gofmm_handle* H, int32_t r) {
+  if (r <= H->ws_r) return;
+  H->d_wp.alloc(size_t(H->ld_wp) * r * sizeof(double));
+  H->d_what.alloc(size_t(H->ld_s) * r * sizeof(double));
+  H->d_c.alloc(size_t(H->ld_s) * r * sizeof(double));
+  H->ws_r = r;
+  H->plan_uploaded = false;
+}
+
+// resolve host groups/terms into device structs against the current workspace pointers
+void upload_plan(gofmm_handle* H) {
+  if (H->plan_uploaded) return;
+  std::vector<Group> gs;
+  std::vector<Term> ts;
+  gs.reserve(H->groups.size());
+  const double* blobs[4] = {H->d_proj.as<double>(), H->d_diag.as<double>(), H->d_near.as<double>(),
+                            H->d_far.as<double>()};
+  const double* xblobs[2] = {H->d_xp.as<double>(), H->d_xs.as<double>()};
+  auto bptr = [&](Buf b) -> std::pair<const double*, int64_t> {
+    switch (b) {
+      case Buf::Wp: return {H->d_wp.as<double>(), H->ld_wp};
+      case Buf::What: return {H->d_what.as<double>(), H->ld_s};
+      case Buf::C: return {H->d_c.as<double>(), H->ld_s};
+      default: return {nullptr, 0};
+    }
+  };
+  for (const HostGroup& hg : H->groups) {
+    Group g{};
+    g.crow = hg.c_row;
+    g.M = hg.M;
+    g.tbeg = int(ts.size());
+    for (const HostTerm& ht : hg.terms) {
+      Term t{};
+      auto [bp, ldb] = bptr(ht.b_buf);
+      t.b = bp + ht.b_row;
+      t.ldb = ldb;
+      t.K = ht.K;
+      if (ht.kind == 1) {
+        t.flags = kTermGen;
+        t.xr = xblobs[ht.x_blob] + ht.xr_off * H->dim;
+        t.xc = xblobs[ht.x_blob] + ht.xc_off * H->dim;
+        t.a = nullptr;
+      } else {
+        t.flags = ht.row_major ? kTermRowMajorA : 0;
+        t.a = blobs[ht.a_blob] + ht.a_off;
+        t.lda = ht.lda;
+      }
+      ts.push_back(t);
+    }
+    g.tend = int(ts.size());
+    gs.push_back(g);
+  }
+  GOFMM_CUDA(cudaMemcpy(H->d_groups.p, gs.data(), gs.size() * sizeof(Group), cudaMemcpyHostToDevice));
+  if (!ts.empty()) GOFMM_CUDA(cudaMemcpy(H->d_terms.p, ts.data(), ts.size() * sizeof(Term), cudaMemcpyHostToDevice));
+  H->plan_uploaded = true;
+}
+
+}  // namespace
+}  // namespace gofmm
+
+namespace gofmm {
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return GOFMM_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_last_error = std::string("host allocation failed: ") + e.what();
+    return GOFMM_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return GOFMM_ERR_INVALID;
+  }
+}
+
+// Enqueue one evaluation on `st`: W (original order, device) -> u_perm (device).
+void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double* d_u, int64_t ldu, cudaStream_t st,
+             bool timed) {
+  ensure_workspace(H, r);
+  upload_plan(H);
+  if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[0], st));
+  {
+    // K5: row gather into the padded leaf layout (evaluate.hpp:294-295)
+    const int cpb = 8;  // columns per block: keeps the gathered source columns L2-resident
+    dim3 grid(unsigned((H->ld_wp + 255) / 256), unsigned((r + cpb - 1) / cpb));
+    permute_rows_in<<<grid, 256, 0, st>>>(d_w, ldw, H->d_prow.as<int32_t>(), H->ld_wp, r, cpb,
+                                          H->d_wp.as<double>(), H->ld_wp);
+  }
+  // ev[1 + p] marks the start of phase p (0 upward, 1 downward, 2 output); ev[4] the end
+  if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[1], st));
+  int marked = 1;
+  for (const Launch& L : H->launches) {
+    while (timed && marked <= L.phase) GOFMM_CUDA(cudaEventRecord(H->ev[1 + marked++], st));
+    double* cbase;
+    int64_t ldc;
+    switch (L.out) {
+      case Buf::What: cbase = H->d_what.as<double>(); ldc = H->ld_s; break;
+      case Buf::C: cbase = H->d_c.as<double>(); ldc = H->ld_s; break;
+      default: cbase = d_u; ldc = ldu; break;
+    }
+    const Tile* tiles = H->d_tiles.as<Tile>() + L.first_tile;
+    if (L.gen) {
+      const int dmax = (H->dim == 1 || H->dim == 2 || H->dim == 3 || H->dim == 4 || H->dim == 6 || H->dim == 8)
+                           ? H->dim
+                           : kMaxDimRt;
+      dim3 grid(unsigned(L.ntiles), unsigned((r + 255) / 256));
+      H->kfn_g<<<grid, ShapeG::kThreads, ShapeG::smem_bytes(dmax), st>>>(
+          tiles, H->d_groups.as<Group>(), H->d_terms.as<Term>(), r, H->kp, cbase, ldc);
+    } else {
+      dim3 grid(unsigned(L.ntiles), unsigned((r + 127) / 128));
+      H->kfn_s<<<grid, ShapeS::kThreads, ShapeS::smem_bytes(0), st>>>(tiles, H->d_groups.as<Group>(),
+                                                                      H->d_terms.as<Term>(), r, H->kp, cbase, ldc);
+    }
+  }
+  if (timed) {
+    while (marked <= 2) GOFMM_CUDA(cudaEventRecord(H->ev[1 + marked++], st));
+    GOFMM_CUDA(cudaEventRecord(H->ev[4], st));
+  }
+  GOFMM_CUDA(cudaGetLastError());
+}
+
+void fill_phase_times(gofmm_handle* H, gofmm_eval_stats* s) {
+  GOFMM_CUDA(cudaEventSynchronize(H->ev[4]));
+  float t[4];
+  for (int i = 0; i < 4; ++i) GOFMM_CUDA(cudaEventElapsedTime(&t[i], H->ev[i], H->ev[i + 1]));
+  s->ms_permute = t[0];
+  s->ms_upward = t[1];
+  s->ms_downward = t[2];
+  s->ms_output = t[3];
+}
+
+void check_args(gofmm_handle* H, const void* w, int64_t ldw, int32_t r, const void* u, int64_t ldu) {
+  if (!H) throw Error(GOFMM_ERR_INVALID, "null handle");
+  // evaluate.hpp:288-289
+  if (r < 1) throw Error(GOFMM_ERR_INVALID, "evaluate: w needs at least one column");
+  if (ldw < H->n) throw Error(GOFMM_ERR_INVALID, "evaluate: w has wrong row count");
+  if (ldu < H->n) throw Error(GOFMM_ERR_INVALID, "evaluate: u has wrong row count");
+  if (!w || !u) throw Error(GOFMM_ERR_INVALID, "evaluate: null buffer");
+}
+
+}  // namespace
+}  // namespace gofmm
+
+using namespace gofmm;
+
+extern "C" {
+
+int32_t gofmm_abi_version(void) { return 1; }
+
+const char* gofmm_last_error(void) { return g_last_error.c_str(); }
+
+int gofmm_create(const gofmm_tree_desc* desc, const gofmm_options* opts, gofmm_handle** out) {
+  return guarded([&] {
+    if (!out) throw Error(GOFMM_ERR_INVALID, "null output handle");
+    *out = nullptr;
+    validate(desc);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw Error(GOFMM_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    auto H = std::make_unique<gofmm_handle>();
+    H->device = opts ? opts->device : 0;
+    GOFMM_CUDA(cudaSetDevice(H->device));
+    GOFMM_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
+    for (auto& e : H->ev) GOFMM_CUDA(cudaEventCreate(&e));
+    build(H.get(), desc, opts);
+    *out = H.release();
+  });
+}
+
+int gofmm_destroy(gofmm_handle* H) {
+  return guarded([&] {
+    if (!H) return;
+    cudaSetDevice(H->device);
+    cudaStreamSynchronize(H->stream);
+    for (auto& e : H->ev)
+      if (e) cudaEventDestroy(e);
+    if (H->stream) cudaStreamDestroy(H->stream);
+    delete H;
+  });
+}
+
+int64_t gofmm_flops(const gofmm_handle* H, int32_t r) { return H ? H->flops_per_rhs * int64_t(r) : -1; }
+
+int32_t gofmm_launches_per_eval(const gofmm_handle* H) { return H ? int32_t(H->launches.size()) + 1 : -1; }
+
+int64_t gofmm_device_bytes(const gofmm_handle* H) {
+  if (!H) return -1;
+  const DevBuf* bufs[] = {&H->d_proj, &H->d_diag, &H->d_near,  &H->d_far,   &H->d_xp,   &H->d_xs,
+                          &H->d_prow, &H->d_iperm, &H->d_tiles, &H->d_groups, &H->d_terms, &H->d_wp,
+                          &H->d_what, &H->d_c,    &H->d_win,   &H->d_uout};
+  int64_t s = 0;
+  for (auto* b : bufs) s += int64_t(b->bytes);
+  return s;
+}
+
+int gofmm_evaluate_device(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double* d_u, int64_t ldu,
+                          void* stream, int32_t stats_sync, gofmm_eval_stats* stats) {
+  return guarded([&] {
+    check_args(H, d_w, ldw, r, d_u, ldu);
+    GOFMM_CUDA(cudaSetDevice(H->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    auto t0 = std::chrono::steady_clock::now();
+    enqueue(H, d_w, ldw, r, d_u, ldu, st, stats && stats_sync);
+    if (stats) {
+      std::memset(stats, 0, sizeof(*stats));
+      stats->flops = H->flops_per_rhs * int64_t(r);
+      if (stats_sync) {
+        fill_phase_times(H, stats);
+        stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      }
+    }
+  });
+}
+
+int gofmm_evaluate(gofmm_handle* H, const double* w, int64_t ldw, int32_t r, double* u_perm, int64_t ldu,
+                   gofmm_eval_stats* stats) {
+  return guarded([&] {
+    check_args(H, w, ldw, r, u_perm, ldu);
+    GOFMM_CUDA(cudaSetDevice(H->device));
+    auto t0 = std::chrono::steady_clock::now();
+    const size_t bytes = size_t(H->n) * r * sizeof(double);
+    if (H->d_win.bytes < bytes) {
+      H->d_win.alloc(bytes, false);
+      H->d_uout.alloc(bytes, false);
+    }
+    cudaStream_t st = H->stream;
+    GOFMM_CUDA(cudaEventRecord(H->ev[5], st));
+    GOFMM_CUDA(cudaMemcpy2DAsync(H->d_win.p, size_t(H->n) * sizeof(double), w, size_t(ldw) * sizeof(double),
+                                 size_t(H->n) * sizeof(double), r, cudaMemcpyHostToDevice, st));
+    GOFMM_CUDA(cudaEventRecord(H->ev[6], st));
+    enqueue(H, H->d_win.as<double>(), H->n, r, H->d_uout.as<double>(), H->n, st, stats != nullptr);
+    GOFMM_CUDA(cudaMemcpy2DAsync(u_perm, size_t(ldu) * sizeof(double), H->d_uout.p, size_t(H->n) * sizeof(double),
+                                 size_t(H->n) * sizeof(double), r, cudaMemcpyDeviceToHost, st));
+    GOFMM_CUDA(cudaEventRecord(H->ev[7], st));
+    GOFMM_CUDA(cudaStreamSynchronize(st));
+    if (stats) {
+      std::memset(stats, 0, sizeof(*stats));
+      stats->flops = H->flops_per_rhs * int64_t(r);
+      fill_phase_times(H, stats);
+      float a, b;
+      GOFMM_CUDA(cudaEventElapsedTime(&a, H->ev[5], H->ev[6]));
+      GOFMM_CUDA(cudaEventElapsedTime(&b, H->ev[4], H->ev[7]));
+      stats->ms_h2d = a;
+      stats->ms_d2h = b;
+      stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+  });
+}
+
+int gofmm_unpermute_device(gofmm_handle* H, const double* d_up, int64_t ldp, int32_t r, double* d_u, int64_t ldu,
+                           void* stream) {
+  return guarded([&] {
+    check_args(H, d_up, ldp, r, d_u, ldu);
+    GOFMM_CUDA(cudaSetDevice(H->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    const int cpb = 8;
+    dim3 grid(unsigned((H->n + 255) / 256), unsigned((r + cpb - 1) / cpb));
+    unpermute_rows<<<grid, 256, 0, st>>>(d_up, ldp, H->d_iperm.as<int32_t>(), H->n, r, cpb, d_u, ldu);
+    GOFMM_CUDA(cudaGetLastError());
+  });
+}
+
+}  // extern "C"

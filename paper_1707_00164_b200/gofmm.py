@@ -1,0 +1,229 @@
+"""Host-side mirror of the reference evaluate API over the C-ABI (include/gofmm_b200.h).
+
+Reference interface replaced (same names, argument meaning and error behaviour):
+    gfmm::Potentials evaluate(const HMatrix&, const Matrix& w, const EvalOptions&)
+        -> Evaluator.evaluate(w)                       evaluate.hpp:287-317
+    gfmm::unpermute(const MetricTree&, const Matrix&) -> Evaluator.unpermute(u_perm)
+                                                       evaluate.hpp:21-25
+    struct Potentials { Matrix u; long long flops; double seconds; }
+                                                       evaluate.hpp:15-19
+The compressed input is the reference HMatrix (compress.hpp:65-79) flattened into
+``CompressedTree``. All compute runs in the sm_100a extension; this module only marshals arrays.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field, fields
+
+import numpy as np
+
+from . import _lib as L
+
+
+@dataclass
+class CompressedTree:
+    """Flattened HMatrix: node table (tree.hpp:13-46), skeletons (compress.hpp:39-47), near/far lists."""
+
+    n: int
+    parent: np.ndarray
+    left: np.ndarray
+    right: np.ndarray
+    level: np.ndarray
+    start: np.ndarray
+    end: np.ndarray
+    iperm: np.ndarray
+    rank: np.ndarray          # -1 = invalid skeleton (root)
+    skel_off: np.ndarray      # [num_nodes+1]
+    skel_idx: np.ndarray
+    proj_off: np.ndarray      # [num_nodes+1]
+    proj: np.ndarray          # per node rank x ncand column-major
+    near_a: np.ndarray
+    near_b: np.ndarray
+    far_a: np.ndarray
+    far_b: np.ndarray
+    coords: np.ndarray | None = None   # d x n original order (kernel sources)
+    kernel: int = -1
+    kparams: tuple = (0.0, 0.0)
+    diag_off: np.ndarray | None = None  # stored sources (DenseOracle-backed trees)
+    diag: np.ndarray | None = None
+    near_off: np.ndarray | None = None
+    near_blk: np.ndarray | None = None
+    far_off: np.ndarray | None = None
+    far_blk: np.ndarray | None = None
+    depth: int = 0
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def num_nodes(self) -> int:
+        return int(self.parent.shape[0])
+
+    @classmethod
+    def from_any(cls, obj) -> "CompressedTree":
+        """Adopt any object with the same field names (e.g. a test oracle's export)."""
+        names = {f.name for f in fields(cls)}
+        return cls(**{k: getattr(obj, k) for k in names if hasattr(obj, k)})
+
+
+@dataclass
+class Potentials:
+    """evaluate.hpp:15-19 — u is N x r in PERMUTED (tree) order."""
+
+    u: np.ndarray
+    flops: int
+    seconds: float
+    stats: dict = field(default_factory=dict)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class Evaluator:
+    """A compressed tree resident on one B200, ready for repeated u = K~ W (gofmm_create)."""
+
+    def __init__(self, tree: CompressedTree, device: int = 0, near_mode: int = L.BLOCKS_MATRIX_FREE,
+                 far_mode: int = L.BLOCKS_MATRIX_FREE, stored: bool | None = None):
+        self.tree = tree
+        self.n = int(tree.n)
+        lib = L.lib()
+        keep = []
+
+        def k(a):
+            keep.append(a)
+            return _p(a)
+
+        d = L.TreeDesc()
+        d.n, d.num_nodes = self.n, tree.num_nodes
+        d.parent, d.left, d.right = k(_i32(tree.parent)), k(_i32(tree.left)), k(_i32(tree.right))
+        d.level, d.start, d.end = k(_i32(tree.level)), k(_i32(tree.start)), k(_i32(tree.end))
+        d.iperm, d.rank = k(_i32(tree.iperm)), k(_i32(tree.rank))
+        d.skel_offset, d.skel_idx = k(_i64(tree.skel_off)), k(_i32(np.append(tree.skel_idx, 0)))
+        d.proj_offset, d.proj = k(_i64(tree.proj_off)), k(_f64(np.append(tree.proj, 0.0)))
+        d.num_near, d.near_a, d.near_b = len(tree.near_a), k(_i32(np.append(tree.near_a, 0))), k(
+            _i32(np.append(tree.near_b, 0)))
+        d.num_far, d.far_a, d.far_b = len(tree.far_a), k(_i32(np.append(tree.far_a, 0))), k(
+            _i32(np.append(tree.far_b, 0)))
+        use_stored = stored if stored is not None else (tree.coords is None or tree.kernel < 0)
+        if use_stored:
+            if tree.diag is None:
+                raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "stored source needs diag/near/far blocks")
+            d.source = L.SOURCE_STORED
+            d.diag_offset, d.diag_blocks = k(_i64(tree.diag_off)), k(_f64(tree.diag))
+            d.near_offset, d.near_blocks = k(_i64(tree.near_off)), k(_f64(tree.near_blk))
+            d.far_offset, d.far_blocks = k(_i64(tree.far_off)), k(_f64(tree.far_blk))
+        else:
+            d.source = L.SOURCE_KERNEL
+            d.kernel = int(tree.kernel)
+            coords = np.asfortranarray(tree.coords, dtype=np.float64)
+            d.dim = int(coords.shape[0])
+            d.coords = k(coords)
+            for i, v in enumerate(tree.kparams[:4]):
+                d.kparam[i] = float(v)
+        o = L.Options(device, near_mode, far_mode, 0)
+        h = C.c_void_p()
+        L.check(lib.gofmm_create(C.byref(d), C.byref(o), C.byref(h)))
+        self._h = h
+        self.stored = use_stored
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.lib().gofmm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ------------------------------------------------------------------ API
+    def flops(self, r: int) -> int:
+        """Reference flop counter (evaluate.hpp:154-214) for r right-hand sides."""
+        return int(L.lib().gofmm_flops(self._h, r))
+
+    @property
+    def launches_per_eval(self) -> int:
+        return int(L.lib().gofmm_launches_per_eval(self._h))
+
+    @property
+    def device_bytes(self) -> int:
+        return int(L.lib().gofmm_device_bytes(self._h))
+
+    def evaluate(self, w: np.ndarray) -> Potentials:
+        """u_perm = K~ w from HOST memory (the drop-in for gfmm::evaluate; evaluate.hpp:287-317)."""
+        w = np.asarray(w, dtype=np.float64)
+        if w.ndim == 1:
+            w = w.reshape(-1, 1)
+        if w.shape[0] != self.n:
+            raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "evaluate: w has wrong row count")
+        if w.shape[1] < 1:
+            raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "evaluate: w needs at least one column")
+        w = np.asfortranarray(w)
+        r = int(w.shape[1])
+        u = np.empty((self.n, r), dtype=np.float64, order="F")
+        st = L.EvalStats()
+        t0 = time.perf_counter()
+        L.check(L.lib().gofmm_evaluate(self._h, _p(w), self.n, r, _p(u), self.n, C.byref(st)))
+        secs = time.perf_counter() - t0
+        return Potentials(u=u, flops=int(st.flops), seconds=secs, stats=_stats(st))
+
+    def evaluate_device(self, w_ptr: int, ldw: int, r: int, u_ptr: int, ldu: int, stream: int = 0,
+                        sync_stats: bool = False) -> dict:
+        """Device-pointer variant (W and u_perm already resident in HBM); enqueues on `stream`."""
+        st = L.EvalStats()
+        L.check(L.lib().gofmm_evaluate_device(self._h, C.c_void_p(w_ptr), ldw, r, C.c_void_p(u_ptr), ldu,
+                                              C.c_void_p(stream) if stream else None, 1 if sync_stats else 0,
+                                              C.byref(st)))
+        return _stats(st)
+
+    def evaluate_torch(self, w, out=None, sync_stats: bool = False):
+        """u_perm = K~ w for CUDA torch tensors (column-major = transposed contiguous views)."""
+        import torch
+
+        if not (w.is_cuda and w.dtype == torch.float64):
+            raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "evaluate_torch: w must be a CUDA float64 tensor")
+        wt = _colmajor(w)
+        r = int(w.shape[1])
+        if out is None:
+            out = torch.empty((r, self.n), dtype=torch.float64, device=w.device).t()
+        stream = torch.cuda.current_stream(w.device).cuda_stream
+        stats = self.evaluate_device(wt.data_ptr(), wt.stride(1), r, out.data_ptr(), out.stride(1), stream,
+                                     sync_stats)
+        return out, stats
+
+    def unpermute(self, u_perm: np.ndarray) -> np.ndarray:
+        """out.row(iperm[t]) = u_perm.row(t) (evaluate.hpp:21-25)."""
+        u_perm = np.asarray(u_perm)
+        out = np.empty_like(u_perm)
+        out[np.asarray(self.tree.iperm, dtype=np.int64)] = u_perm
+        return out
+
+
+def _colmajor(t):
+    """Return t if it is column-major (stride(0)==1), else a column-major copy."""
+    if t.dim() == 2 and t.stride(0) == 1 and t.stride(1) >= t.shape[0]:
+        return t
+    return t.t().contiguous().t()
+
+
+def _stats(st: L.EvalStats) -> dict:
+    return {name: getattr(st, name) for name, _ in L.EvalStats._fields_}
