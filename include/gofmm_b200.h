@@ -133,6 +133,10 @@ int gofmm_unpermute_device(gofmm_handle* h, const double* d_u_perm, int64_t ldp,
 /* Reference flop count (Potentials::flops) for r right-hand sides, without evaluating. */
 int64_t gofmm_flops(const gofmm_handle* h, int32_t r);
 
+/* Reference flops split by phase for r right-hand sides: out3 = {upward (N2S),
+ * downward (S2S + S2N), output (L2L + leaf S2N)}. */
+int gofmm_phase_flops(const gofmm_handle* h, int32_t r, int64_t* out3);
+
 /* Bytes of device memory held by the handle (tree + workspace). */
 int64_t gofmm_device_bytes(const gofmm_handle* h);
 

@@ -415,12 +415,13 @@ int gfmm_ref_import(const gfmm_ref_import_args* a, gfmm_ref** out) {
 
 // evaluate() (evaluate.hpp:287-317): w is n x r original order, u_perm receives the permuted
 // potentials. mode: 0 LevelByLevel, 1 TaskDag.
-int gfmm_ref_evaluate(const gfmm_ref* ref, const double* w, int32_t r, double* u_perm, int32_t mode,
-                      int32_t threads, int64_t* flops, double* seconds) {
+// nrows is w's row count: a mismatch reaches evaluate() and throws there (evaluate.hpp:288).
+int gfmm_ref_evaluate(const gfmm_ref* ref, const double* w, int32_t nrows, int32_t r, double* u_perm,
+                      int32_t mode, int32_t threads, int64_t* flops, double* seconds) {
   return guarded([&] {
     const HMatrix& h = ref->h;
-    Matrix wm(h.n, r);
-    if (h.n && r > 0) std::memcpy(wm.data(), w, sizeof(double) * size_t(h.n) * size_t(r));
+    Matrix wm(nrows, r);
+    if (nrows && r > 0) std::memcpy(wm.data(), w, sizeof(double) * size_t(nrows) * size_t(r));
     EvalOptions o;
     o.mode = mode == 0 ? TraversalMode::LevelByLevel : TraversalMode::TaskDag;
     o.threads = threads;

@@ -126,7 +126,7 @@ def lib():
         L.gfmm_ref_get_sizes.argtypes = [_P, C.POINTER(_Sizes)]
         L.gfmm_ref_export.argtypes = [_P, C.POINTER(_ExportArgs)]
         L.gfmm_ref_import.argtypes = [C.POINTER(_ImportArgs), C.POINTER(_P)]
-        L.gfmm_ref_evaluate.argtypes = [_P, _P, C.c_int32, _P, C.c_int32, C.c_int32,
+        L.gfmm_ref_evaluate.argtypes = [_P, _P, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32,
                                         C.POINTER(C.c_int64), C.POINTER(C.c_double)]
         L.gfmm_ref_unpermute.argtypes = [_P, _P, C.c_int32, _P]
         L.gfmm_ref_error_eps2.argtypes = [_P, C.c_int32, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
@@ -283,7 +283,7 @@ class RefHMatrix:
             w = w.reshape(-1, 1, order="F")
         u = np.empty_like(w, order="F")
         fl, sec = C.c_int64(), C.c_double()
-        _check(lib().gfmm_ref_evaluate(self._h, _ptr(w), w.shape[1], _ptr(u), mode, threads,
+        _check(lib().gfmm_ref_evaluate(self._h, _ptr(w), w.shape[0], w.shape[1], _ptr(u), mode, threads,
                                        C.byref(fl), C.byref(sec)))
         return u, fl.value, sec.value
 

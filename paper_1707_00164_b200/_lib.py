@@ -95,7 +95,7 @@ _lib = None
 
 # every symbol include/gofmm_b200.h declares
 EXPORTS = ("gofmm_create", "gofmm_evaluate", "gofmm_evaluate_device", "gofmm_unpermute_device",
-           "gofmm_flops", "gofmm_device_bytes", "gofmm_launches_per_eval", "gofmm_destroy",
+           "gofmm_flops", "gofmm_phase_flops", "gofmm_device_bytes", "gofmm_launches_per_eval", "gofmm_destroy",
            "gofmm_last_error", "gofmm_abi_version")
 
 
@@ -113,6 +113,7 @@ def lib():
         L.gofmm_unpermute_device.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, P]
         L.gofmm_flops.argtypes = [P, C.c_int32]
         L.gofmm_flops.restype = C.c_int64
+        L.gofmm_phase_flops.argtypes = [P, C.c_int32, P]
         L.gofmm_device_bytes.argtypes = [P]
         L.gofmm_device_bytes.restype = C.c_int64
         L.gofmm_launches_per_eval.argtypes = [P]

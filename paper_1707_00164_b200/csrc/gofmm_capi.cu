@@ -207,6 +207,7 @@ struct gofmm_handle {
 
   gofmm::KernelFn kfn_s = nullptr, kfn_g = nullptr;
   int64_t flops_per_rhs = 0;
+  int64_t phase_flops_per_rhs[3] = {0, 0, 0};  // upward, downward, output
 };
 
 namespace gofmm {
@@ -531,6 +532,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
         t.K = int(pad2(H->rank[H->left[i]]) + pad2(H->rank[H->right[i]]));
       }
       flops += 2LL * H->rank[i] * ncand[i];
+      H->phase_flops_per_rhs[0] += 2LL * H->rank[i] * ncand[i];
       g.terms.push_back(t);
       gs.push_back(std::move(g));
     }
@@ -565,6 +567,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
           t.row_major = p.transposed;
         }
         flops += 2LL * H->rank[i] * H->rank[p.other];
+        H->phase_flops_per_rhs[1] += 2LL * H->rank[i] * H->rank[p.other];
         g.terms.push_back(t);
       }
       const int par = H->parent[i];
@@ -580,6 +583,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
         t.b_row = H->soff[par];
         t.K = H->rank[par];
         flops += 2LL * H->rank[par] * H->rank[i];
+        H->phase_flops_per_rhs[1] += 2LL * H->rank[par] * H->rank[i];
         g.terms.push_back(t);
       }
       gs.push_back(std::move(g));
@@ -652,6 +656,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     push_launch(gs, gen_near, Buf::Out, 2);
   }
   H->flops_per_rhs = flops;
+  H->phase_flops_per_rhs[2] = flops - H->phase_flops_per_rhs[0] - H->phase_flops_per_rhs[1];
 
   H->kfn_s = &grouped_gemm_f64<CFG_S, kKindNone, 1>;
   size_t smem_s = ShapeS::smem_bytes(0);
@@ -859,6 +864,13 @@ int gofmm_destroy(gofmm_handle* H) {
 }
 
 int64_t gofmm_flops(const gofmm_handle* H, int32_t r) { return H ? H->flops_per_rhs * int64_t(r) : -1; }
+
+int gofmm_phase_flops(const gofmm_handle* H, int32_t r, int64_t* out3) {
+  return guarded([&] {
+    if (!H || !out3) throw Error(GOFMM_ERR_INVALID, "null argument");
+    for (int i = 0; i < 3; ++i) out3[i] = H->phase_flops_per_rhs[i] * int64_t(r);
+  });
+}
 
 int32_t gofmm_launches_per_eval(const gofmm_handle* H) { return H ? int32_t(H->launches.size()) + 1 : -1; }
 

@@ -160,6 +160,12 @@ class Evaluator:
         """Reference flop counter (evaluate.hpp:154-214) for r right-hand sides."""
         return int(L.lib().gofmm_flops(self._h, r))
 
+    def phase_flops(self, r: int) -> dict:
+        """Reference flops split by phase: upward (N2S), downward (S2S+S2N), output (L2L+leaf S2N)."""
+        out = np.zeros(3, dtype=np.int64)
+        L.check(L.lib().gofmm_phase_flops(self._h, r, _p(out)))
+        return dict(upward=int(out[0]), downward=int(out[1]), output=int(out[2]))
+
     @property
     def launches_per_eval(self) -> int:
         return int(L.lib().gofmm_launches_per_eval(self._h))
@@ -168,8 +174,9 @@ class Evaluator:
     def device_bytes(self) -> int:
         return int(L.lib().gofmm_device_bytes(self._h))
 
-    def evaluate(self, w: np.ndarray) -> Potentials:
-        """u_perm = K~ w from HOST memory (the drop-in for gfmm::evaluate; evaluate.hpp:287-317)."""
+    def evaluate(self, w: np.ndarray, out: np.ndarray | None = None) -> Potentials:
+        """u_perm = K~ w from HOST memory (the drop-in for gfmm::evaluate; evaluate.hpp:287-317).
+        `out` (optional, N x r Fortran-ordered, e.g. a pinned buffer) receives u_perm."""
         w = np.asarray(w, dtype=np.float64)
         if w.ndim == 1:
             w = w.reshape(-1, 1)
@@ -179,7 +186,12 @@ class Evaluator:
             raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "evaluate: w needs at least one column")
         w = np.asfortranarray(w)
         r = int(w.shape[1])
-        u = np.empty((self.n, r), dtype=np.float64, order="F")
+        if out is None:
+            u = np.empty((self.n, r), dtype=np.float64, order="F")
+        else:
+            u = out
+            if u.shape != (self.n, r) or u.dtype != np.float64 or not u.flags.f_contiguous:
+                raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "evaluate: out must be N x r float64 Fortran order")
         st = L.EvalStats()
         t0 = time.perf_counter()
         L.check(L.lib().gofmm_evaluate(self._h, _p(w), self.n, r, _p(u), self.n, C.byref(st)))
@@ -190,8 +202,10 @@ class Evaluator:
                         sync_stats: bool = False) -> dict:
         """Device-pointer variant (W and u_perm already resident in HBM); enqueues on `stream`."""
         st = L.EvalStats()
+        # torch's default stream is the legacy NULL stream: pass cudaStreamLegacy (0x1) explicitly,
+        # because NULL selects the handle's own stream in the C-ABI
         L.check(L.lib().gofmm_evaluate_device(self._h, C.c_void_p(w_ptr), ldw, r, C.c_void_p(u_ptr), ldu,
-                                              C.c_void_p(stream) if stream else None, 1 if sync_stats else 0,
+                                              C.c_void_p(stream if stream else 1), 1 if sync_stats else 0,
                                               C.byref(st)))
         return _stats(st)
 

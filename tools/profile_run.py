@@ -1,0 +1,32 @@
+"""Profiling driver: a c3-shaped workload (default N=2^18, same d/m/s/budget/r) evaluated twice,
+for `ncu` captures of the grouped GEMM launches (see profiles/README.md for the commands)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_1707_00164_b200 import Evaluator, synth  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c3")
+ap.add_argument("--n", type=int, default=1 << 18)
+ap.add_argument("--budget", type=float, default=None)
+ap.add_argument("--evals", type=int, default=2)
+ap.add_argument("--far-mode", type=int, default=0)
+ap.add_argument("--near-mode", type=int, default=0)
+a = ap.parse_args()
+over = {"n": a.n}
+if a.budget is not None:
+    over["budget"] = a.budget
+tree, cfg = synth.make_config_tree(a.config, **over)
+ev = Evaluator(tree, near_mode=a.near_mode, far_mode=a.far_mode)
+r = cfg["r"]
+w = torch.randn((r, tree.n), dtype=torch.float64, device="cuda").t()
+u = torch.empty((r, tree.n), dtype=torch.float64, device="cuda").t()
+for i in range(a.evals):
+    _, st = ev.evaluate_torch(w, out=u, sync_stats=True)
+    print(i, {k: round(v, 3) for k, v in st.items()}, ev.phase_flops(r), flush=True)
+print("launches/eval", ev.launches_per_eval, "depth", tree.depth)
