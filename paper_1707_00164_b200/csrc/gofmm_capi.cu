@@ -15,6 +15,8 @@
 //                    Siblings are adjacent, so [what_l; what_r] is one contiguous row range.
 //   proj_a         : k_a x ncand_pad column-major, ld = pad2(k_a); interior proj gets a zero
 //                    column after each odd-rank child so its columns line up with skeleton space.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -79,23 +81,30 @@ struct DevBuf {
 };
 
 // ---------------------------------------------------------------- kernel configurations
-// S: stored-operand GEMMs (N2S / downward / output without generation).
-// G: generated-operand GEMMs (matrix-free L2L and S2S): warps split M only, so every A entry is
-//    generated exactly once per CTA, and BN is wide to amortise exp() over the RHS columns.
-constexpr int kBK = 16, kStages = 3, kBM_S = 128, kBM_G = 64;
-#define CFG_S kBM_S, 128, 4, 2, kBK, kStages
-#define CFG_G kBM_G, 256, 8, 1, kBK, kStages
-using ShapeS = GemmShape<CFG_S>;
-using ShapeG = GemmShape<CFG_G>;
+// S: stored-operand GEMMs (N2S / downward / output without generation): 128x128 CTA tile,
+//    8 consumer warps of 32x64.
+// G: generated-operand GEMMs (matrix-free L2L and S2S): 64x256 CTA tile, 8 consumer warps of
+//    8x256 — warps split M only, so every A entry is generated exactly once per CTA, and BN is
+//    wide to amortise exp() over the RHS columns.
+constexpr int kStages = 4, kBM_S = 128, kBN_S = 128, kBM_G = 64, kBN_G = 256;
+#define CFG_S kBM_S, kBN_S, 4, 2, kStages
+#define CFG_G kBM_G, kBN_G, 8, 1, kStages
+constexpr int kThreadsS = kProducerThreads + 4 * 2 * 32;
+constexpr int kThreadsG = kProducerThreads + 8 * 1 * 32;
 
-using KernelFn = void (*)(const Tile*, const Group*, const Term*, int32_t, KernelParams, double*, int64_t);
+using KernelFn = void (*)(BMaps, const Tile*, const Group*, const Term*, int32_t, KernelParams, double*, int64_t);
+
+struct GenKernel {
+  KernelFn fn;
+  size_t smem;
+};
 
 template <int KIND, int DIM>
-KernelFn gen_kernel() {
-  return &grouped_gemm_f64<CFG_G, KIND, DIM>;
+GenKernel gen_kernel() {
+  return {&grouped_gemm_f64<CFG_G, KIND, DIM>, gemm_smem_bytes<CFG_G, KIND, DIM>()};
 }
 
-KernelFn pick_gen_kernel(int kind, int dim) {
+GenKernel pick_gen_kernel(int kind, int dim) {
 #define GOFMM_DIMS(K)                        \
   switch (dim) {                             \
     case 1: return gen_kernel<K, 1>();       \
@@ -114,6 +123,32 @@ KernelFn pick_gen_kernel(int kind, int dim) {
   }
 #undef GOFMM_DIMS
   throw Error(GOFMM_ERR_INVALID, "unsupported kernel id " + std::to_string(kind));
+}
+
+// TMA descriptor encoding through the runtime's driver entry point (no libcuda link needed)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    GOFMM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw Error(GOFMM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// B operand view of a column-major (ld x r) FP64 buffer: boxes of 16 rows x bn columns,
+// 128-byte swizzle (conflict-free fragment loads), out-of-range rows/columns read as zero.
+void encode_bmap(CUtensorMap* map, const double* ptr, int64_t ld, int32_t r, int bn) {
+  cuuint64_t dims[2] = {cuuint64_t(ld), cuuint64_t(r)};
+  cuuint64_t strides[1] = {cuuint64_t(ld) * sizeof(double)};
+  cuuint32_t box[2] = {cuuint32_t(kBK), cuuint32_t(bn)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult rc = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims,
+                                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) throw Error(GOFMM_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(rc)));
 }
 
 template <int KIND, int DIM>
@@ -206,6 +241,9 @@ struct gofmm_handle {
   int32_t ws_r = 0;
 
   gofmm::KernelFn kfn_s = nullptr, kfn_g = nullptr;
+  size_t smem_s = 0, smem_g = 0;
+  gofmm::BMaps maps_s{}, maps_g{};
+  int32_t maps_r = 0;  // r the tensor maps were encoded for
   int64_t flops_per_rhs = 0;
   int64_t phase_flops_per_rhs[3] = {0, 0, 0};  // upward, downward, output
 };
@@ -659,15 +697,13 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   H->phase_flops_per_rhs[2] = flops - H->phase_flops_per_rhs[0] - H->phase_flops_per_rhs[1];
 
   H->kfn_s = &grouped_gemm_f64<CFG_S, kKindNone, 1>;
-  size_t smem_s = ShapeS::smem_bytes(0);
-  GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_s)));
+  H->smem_s = gemm_smem_bytes<CFG_S, kKindNone, 1>();
+  GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_s)));
   if (!stored && (gen_near || gen_far)) {
-    H->kfn_g = pick_gen_kernel(H->kernel, H->dim);
-    const int dmax = (H->dim == 1 || H->dim == 2 || H->dim == 3 || H->dim == 4 || H->dim == 6 || H->dim == 8)
-                         ? H->dim
-                         : kMaxDimRt;
-    size_t smem_g = ShapeG::smem_bytes(dmax);
-    GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_g, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_g)));
+    GenKernel gk = pick_gen_kernel(H->kernel, H->dim);
+    H->kfn_g = gk.fn;
+    H->smem_g = gk.smem;
+    GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_g, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_g)));
   }
   H->d_tiles.upload(H->tiles);
   H->d_groups.alloc(H->groups.size() * sizeof(Group), false);
@@ -683,6 +719,7 @@ void ensure_workspace(gofmm_handle* H, int32_t r) {
   H->d_c.alloc(size_t(H->ld_s) * r * sizeof(double));
   H->ws_r = r;
   H->plan_uploaded = false;
+  H->maps_r = 0;
 }
 
 // resolve host groups/terms into device structs against the current workspace pointers
@@ -694,12 +731,11 @@ void upload_plan(gofmm_handle* H) {
   const double* blobs[4] = {H->d_proj.as<double>(), H->d_diag.as<double>(), H->d_near.as<double>(),
                             H->d_far.as<double>()};
   const double* xblobs[2] = {H->d_xp.as<double>(), H->d_xs.as<double>()};
-  auto bptr = [&](Buf b) -> std::pair<const double*, int64_t> {
+  auto bid = [](Buf b) {
     switch (b) {
-      case Buf::Wp: return {H->d_wp.as<double>(), H->ld_wp};
-      case Buf::What: return {H->d_what.as<double>(), H->ld_s};
-      case Buf::C: return {H->d_c.as<double>(), H->ld_s};
-      default: return {nullptr, 0};
+      case Buf::Wp: return int32_t(kBufWp);
+      case Buf::What: return int32_t(kBufWhat);
+      default: return int32_t(kBufC);
     }
   };
   for (const HostGroup& hg : H->groups) {
@@ -709,9 +745,8 @@ void upload_plan(gofmm_handle* H) {
     g.tbeg = int(ts.size());
     for (const HostTerm& ht : hg.terms) {
       Term t{};
-      auto [bp, ldb] = bptr(ht.b_buf);
-      t.b = bp + ht.b_row;
-      t.ldb = ldb;
+      t.bbuf = bid(ht.b_buf);
+      t.b_row = ht.b_row;
       t.K = ht.K;
       if (ht.kind == 1) {
         t.flags = kTermGen;
@@ -762,6 +797,16 @@ void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double*
              bool timed) {
   ensure_workspace(H, r);
   upload_plan(H);
+  if (H->maps_r != r) {
+    // B operand tensor maps over the workspace buffers for this column count
+    const double* bufs[3] = {H->d_wp.as<double>(), H->d_what.as<double>(), H->d_c.as<double>()};
+    const int64_t lds[3] = {H->ld_wp, H->ld_s, H->ld_s};
+    for (int b = 0; b < 3; ++b) {
+      encode_bmap(&H->maps_s.m[b], bufs[b], lds[b], r, kBN_S);
+      encode_bmap(&H->maps_g.m[b], bufs[b], lds[b], r, kBN_G);
+    }
+    H->maps_r = r;
+  }
   if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[0], st));
   {
     // K5: row gather into the padded leaf layout (evaluate.hpp:294-295)
@@ -784,16 +829,13 @@ void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double*
     }
     const Tile* tiles = H->d_tiles.as<Tile>() + L.first_tile;
     if (L.gen) {
-      const int dmax = (H->dim == 1 || H->dim == 2 || H->dim == 3 || H->dim == 4 || H->dim == 6 || H->dim == 8)
-                           ? H->dim
-                           : kMaxDimRt;
-      dim3 grid(unsigned(L.ntiles), unsigned((r + 255) / 256));
-      H->kfn_g<<<grid, ShapeG::kThreads, ShapeG::smem_bytes(dmax), st>>>(
-          tiles, H->d_groups.as<Group>(), H->d_terms.as<Term>(), r, H->kp, cbase, ldc);
+      dim3 grid(unsigned(L.ntiles), unsigned((r + kBN_G - 1) / kBN_G));
+      H->kfn_g<<<grid, kThreadsG, H->smem_g, st>>>(H->maps_g, tiles, H->d_groups.as<Group>(), H->d_terms.as<Term>(),
+                                                    r, H->kp, cbase, ldc);
     } else {
-      dim3 grid(unsigned(L.ntiles), unsigned((r + 127) / 128));
-      H->kfn_s<<<grid, ShapeS::kThreads, ShapeS::smem_bytes(0), st>>>(tiles, H->d_groups.as<Group>(),
-                                                                      H->d_terms.as<Term>(), r, H->kp, cbase, ldc);
+      dim3 grid(unsigned(L.ntiles), unsigned((r + kBN_S - 1) / kBN_S));
+      H->kfn_s<<<grid, kThreadsS, H->smem_s, st>>>(H->maps_s, tiles, H->d_groups.as<Group>(), H->d_terms.as<Term>(),
+                                                    r, H->kp, cbase, ldc);
     }
   }
   if (timed) {

@@ -12,25 +12,35 @@
 // A operands are either stored (proj, materialised blocks; column- or row-major) or GENERATED
 // in registers from point coordinates (matrix-free L2L / S2S: K_ij of oracle.hpp:148-192).
 //
-// Math: FP64 DMMA (mma.sync.m8n8k4.f64 -> SASS DMMA.8; tcgen05 has no f64 kind), operands
-// staged global->shared with cp.async multi-stage pipelines, accumulators in registers.
+// Blackwell mapping (tcgen05 has no f64 kind; FP64 tensor math is DMMA via mma.sync):
+//   * one PRODUCER warp per CTA: lane 0 streams the B tiles (W_perm / what / c column blocks)
+//     with TMA (cp.async.bulk.tensor, 128B swizzle) and the 32 lanes stage stored A tiles and
+//     point coordinates with cp.async; both complete on a per-stage mbarrier;
+//   * NC CONSUMER warps: fragment loads from shared memory + mma.sync.m8n8k4.f64 (SASS DMMA.8),
+//     accumulators in registers, release the stage through an "empty" mbarrier;
+//   * no __syncthreads in the main loop, so the MMA pipe never waits on address math.
 #pragma once
+
+#include <cuda.h>
 
 #include <cstdint>
 
 namespace gofmm {
 
 enum : int32_t { kTermRowMajorA = 1, kTermGen = 2 };
+// B buffer ids (tensor maps passed per launch): W_perm, what, c
+enum : int32_t { kBufWp = 0, kBufWhat = 1, kBufC = 2 };
 
 struct Term {
   const double* a;   // stored A (nullptr when generated)
-  const double* b;   // B: K x R column-major, ldb
   const double* xr;  // generated: row points, point-major (dim doubles per point)
   const double* xc;  // generated: column points
   int64_t lda;
-  int64_t ldb;
+  int64_t b_row;  // first row of B (K x R) inside buffer `bbuf`
   int32_t K;
-  int32_t flags;
+  int32_t flags;  // kTermRowMajorA | kTermGen
+  int32_t bbuf;   // kBufWp / kBufWhat / kBufC
+  int32_t pad;
 };
 
 struct Group {
@@ -53,6 +63,10 @@ struct KernelParams {
   double p1;  // laplace: exponent (d-2); polynomial: degree
   int32_t dim;
   int32_t pad;
+};
+
+struct BMaps {
+  CUtensorMap m[3];  // indexed by kBuf*
 };
 
 // ------------------------------------------------------------------ reduction order
@@ -120,188 +134,249 @@ constexpr int kMaxDimRt = 16;
 // K(x_i, x_j) exactly as the reference generators build it (oracle.hpp:148-218).
 template <int KIND, int DIM>
 __device__ __forceinline__ double kernel_entry(const double* xi, const double* xj, const KernelParams& kp) {
+  double t[DIM > 0 ? DIM : kMaxDimRt];
+  const int dim = DIM > 0 ? DIM : kp.dim;
   if constexpr (KIND == kPolynomial) {
-    double t[DIM > 0 ? DIM : kMaxDimRt];
-    if constexpr (DIM > 0) {
 #pragma unroll
-      for (int q = 0; q < DIM; ++q) t[q] = xi[q] * xj[q];
-      return pow(eigen_redux<DIM>(t) + kp.p0, kp.p1);
-    } else {
-      for (int q = 0; q < kp.dim; ++q) t[q] = xi[q] * xj[q];
-      return pow(eigen_redux_rt(t, kp.dim) + kp.p0, kp.p1);
-    }
+    for (int q = 0; q < (DIM > 0 ? DIM : kMaxDimRt); ++q)
+      if (DIM > 0 || q < dim) t[q] = xi[q] * xj[q];
+    const double ip = DIM > 0 ? eigen_redux<(DIM > 0 ? DIM : 1)>(t) : eigen_redux_rt(t, dim);
+    return pow(ip + kp.p0, kp.p1);
   } else {
-    double t[DIM > 0 ? DIM : kMaxDimRt];
-    double d2;
-    if constexpr (DIM > 0) {
 #pragma unroll
-      for (int q = 0; q < DIM; ++q) {
-        double e = xi[q] - xj[q];
+    for (int q = 0; q < (DIM > 0 ? DIM : kMaxDimRt); ++q)
+      if (DIM > 0 || q < dim) {
+        const double e = xi[q] - xj[q];
         t[q] = e * e;
       }
-      d2 = eigen_redux<DIM>(t);
-    } else {
-      for (int q = 0; q < kp.dim; ++q) {
-        double e = xi[q] - xj[q];
-        t[q] = e * e;
-      }
-      d2 = eigen_redux_rt(t, kp.dim);
-    }
+    const double d2 = DIM > 0 ? eigen_redux<(DIM > 0 ? DIM : 1)>(t) : eigen_redux_rt(t, dim);
     if constexpr (KIND == kGaussian) {
       return exp(-d2 * kp.p0);
     } else if constexpr (KIND == kExponential) {
       return exp(-sqrt(d2) * kp.p0);
     } else {  // kLaplace: max(|d|, delta)^-(d-2)
-      double rr = fmax(sqrt(d2), kp.p0);
-      return pow(rr, -kp.p1);
+      return pow(fmax(sqrt(d2), kp.p0), -kp.p1);
     }
   }
 }
 
-// ------------------------------------------------------------------ async copy / DMMA helpers
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
-  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  int sz = valid ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+// explicit shared-window loads: the 1024-byte-aligned carve-up of dynamic shared memory hides
+// the address space from the compiler, which would otherwise emit generic LD instructions
+__device__ __forceinline__ double lds64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(gmem), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* gmem, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(gmem), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+// arrive once this thread's prior cp.async copies have landed (counts toward the init count)
+__device__ __forceinline__ void mbar_cp_async_arrive(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
 }
 
 // D(8x8) += A(8x4, row) * B(4x8, col): lane holds A[lane/4][lane%4], B[lane%4][lane/4],
 // D[lane/4][2*(lane%4) + {0,1}].
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
 
 // ------------------------------------------------------------------ grouped multi-term GEMM
-template <int BM, int BN, int WM, int WN, int BK, int STAGES>
+constexpr int kBK = 16;  // k-depth per stage: one 128-byte TMA row of FP64
+
+// Warp roles: warpgroup 0 = producer (4 warps; lane 0 of warp 0 issues TMA, all 128 threads
+// stage cp.async operands), warpgroups 1..2 = 8 consumer warps. setmaxnreg moves registers from
+// the producer (56) to the consumers (224): with 12 resident warps (3 per SM sub-partition) the
+// launch budget is 168 per thread, too few for 64 FP64 accumulators without spills.
+constexpr int kProducerThreads = 128;
+constexpr int kProducerRegs = 56, kConsumerRegs = 224;
+
+template <int BM, int BN, int WM, int WN, int STAGES, int XD>
 struct GemmShape {
-  static constexpr int kThreads = WM * WN * 32;
+  static constexpr int kConsumers = WM * WN;
+  static_assert(kConsumers == 8, "two consumer warpgroups");
+  static constexpr int kThreads = kProducerThreads + kConsumers * 32;
   static constexpr int WTM = BM / WM, WTN = BN / WN;
   static constexpr int MT = WTM / 8, NT = WTN / 8;
-  static constexpr int SA_COL = BM + 4;  // A column-major tile: [BK][BM+4] (m contiguous)
-  static constexpr int SA_ROW = BK + 4;  // A row-major tile:    [BM][BK+4] (k contiguous)
-  static constexpr int A_STAGE = (BK * SA_COL > BM * SA_ROW) ? BK * SA_COL : BM * SA_ROW;
-  static constexpr int SB = BK + 4;  // B tile: [BN][BK+4]
-  static constexpr int B_STAGE = BN * SB;
-  static_assert(BK % 4 == 0 && BM % (8 * WM) == 0 && BN % (8 * WN) == 0, "tile shape");
-  // padding of 4 doubles (8 banks) makes every half-warp fragment load conflict-free
-  static_assert((SA_COL % 16) == 4 && (SB % 16) == 4 && (SA_ROW % 16) == 4, "bank padding");
-  static constexpr size_t smem_bytes(int maxdim) {
-    return sizeof(double) * (size_t(STAGES) * (A_STAGE + B_STAGE) + size_t(STAGES) * BK * maxdim +
-                             size_t(BM) * maxdim);
-  }
+  static constexpr int SA_COL = BM + 4;   // stored A column-major tile [BK][BM+4] (m contiguous)
+  static constexpr int SA_ROW = kBK + 4;  // stored A row-major tile    [BM][BK+4] (k contiguous)
+  static constexpr int A_STAGE = (kBK * SA_COL > BM * SA_ROW) ? kBK * SA_COL : BM * SA_ROW;  // doubles
+  static constexpr int B_STAGE_BYTES = BN * kBK * 8;  // TMA box, 128B-swizzled rows, 1024B aligned
+  static constexpr int X_STAGE = kBK * XD;            // column coordinates (generated terms)
+  static_assert(BM % (8 * WM) == 0 && BN % (8 * WN) == 0 && BN <= 256, "tile shape");
+  static_assert(B_STAGE_BYTES % 1024 == 0, "swizzle-128B tiles need 1024-byte multiples");
+  static constexpr size_t smem_bytes =
+      1024 /* alignment slack */ + size_t(STAGES) * B_STAGE_BYTES + size_t(STAGES) * A_STAGE * 8 +
+      size_t(STAGES) * X_STAGE * 8 + size_t(2 * STAGES) * 8;
 };
 
-template <int BM, int BN, int WM, int WN, int BK, int STAGES, int KIND, int DIM>
-__global__ void __launch_bounds__(WM* WN * 32)
-    grouped_gemm_f64(const Tile* __restrict__ tiles, const Group* __restrict__ groups,
-                     const Term* __restrict__ terms, int32_t R, KernelParams kp, double* __restrict__ cbase,
-                     int64_t ldc) {
-  using S = GemmShape<BM, BN, WM, WN, BK, STAGES>;
-  constexpr int NTH = S::kThreads;
-  constexpr bool kGen = (KIND != kKindNone);
-  constexpr int XD = kGen ? (DIM > 0 ? DIM : kMaxDimRt) : 0;  // coordinate stride in smem
+template <int BM, int BN, int WM, int WN, int STAGES, int KIND, int DIM>
+constexpr size_t gemm_smem_bytes() {
+  constexpr int XD = (KIND != kKindNone) ? (DIM > 0 ? DIM + 1 : kMaxDimRt + 1) : 0;
+  return GemmShape<BM, BN, WM, WN, STAGES, XD>::smem_bytes;
+}
 
-  extern __shared__ __align__(16) double smem[];
-  double* sA = smem;
-  double* sB = sA + STAGES * S::A_STAGE;
-  double* sXc = sB + STAGES * S::B_STAGE;  // [STAGES][BK][XD]
-  double* sXr = sXc + STAGES * BK * XD;    // [BM][XD]
+// byte offset of element (n, k) in a 128B-swizzled [BN][16] FP64 tile
+__device__ __forceinline__ uint32_t swz128(int n, int k) {
+  return uint32_t(n) * 128u + ((uint32_t((k >> 1) ^ (n & 7)) << 4) | (uint32_t(k & 1) << 3));
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES, int KIND, int DIM>
+__global__ void __launch_bounds__(kProducerThreads + WM * WN * 32, 1)
+    grouped_gemm_f64(const __grid_constant__ BMaps maps, const Tile* __restrict__ tiles,
+                     const Group* __restrict__ groups, const Term* __restrict__ terms, int32_t R, KernelParams kp,
+                     double* __restrict__ cbase, int64_t ldc) {
+  constexpr bool kGen = (KIND != kKindNone);
+  constexpr int XD = kGen ? (DIM > 0 ? DIM + 1 : kMaxDimRt + 1) : 0;  // odd stride: no bank conflicts
+  using S = GemmShape<BM, BN, WM, WN, STAGES, XD>;
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sB = base;                                                  // [STAGES][BN*128B]
+  double* sA = reinterpret_cast<double*>(sB + STAGES * S::B_STAGE_BYTES);    // [STAGES][A_STAGE]
+  double* sX = sA + STAGES * S::A_STAGE;                                     // [STAGES][BK][XD]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sX + STAGES * S::X_STAGE);    // full[STAGES], empty[STAGES]
 
   const Tile tile = tiles[blockIdx.x];
   const Group grp = groups[tile.group];
   const int m0 = tile.m0;
   const int n0 = blockIdx.y * BN;
   const int M = grp.M;
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, tig = lane & 3;
-  const int wm0 = (warp / WN) * S::WTM;
-  const int wn0 = (warp % WN) * S::WTN;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int dim = (DIM > 0) ? DIM : kp.dim;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&bars[s]), kProducerThreads + 1);  // producer cp.async arrivals + 1 expect_tx
+      mbar_init(smem_u32(&bars[STAGES + s]), S::kConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
 
   // total pipeline steps across all terms
   int total = 0;
-  for (int t = grp.tbeg; t < grp.tend; ++t) total += (terms[t].K + BK - 1) / BK;
+  for (int t = grp.tbeg; t < grp.tend; ++t) total += (terms[t].K + kBK - 1) / kBK;
 
-  // row coordinates of generated terms (shared by every generated term of the group)
-  if constexpr (kGen) {
-    const double* xr = nullptr;
-    for (int t = grp.tbeg; t < grp.tend; ++t)
-      if (terms[t].flags & kTermGen) {
-        xr = terms[t].xr;
-        break;
+  if (threadIdx.x < kProducerThreads) {
+    // =========================== PRODUCER WARPGROUP ===========================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
+    const int pth = threadIdx.x;
+    int pt = grp.tbeg, pk = 0;
+    while (pt < grp.tend && terms[pt].K == 0) ++pt;
+    for (int s = 0; s < total; ++s) {
+      const int stage = s % STAGES;
+      const uint32_t full = smem_u32(&bars[stage]);
+      mbar_wait(smem_u32(&bars[STAGES + stage]), ((s / STAGES) & 1) ^ 1);
+      const Term T = terms[pt];
+      const int k0 = pk;
+      if (pth == 0) {
+        mbar_arrive_expect_tx(full, S::B_STAGE_BYTES);
+        tma_load_2d(smem_u32(sB + stage * S::B_STAGE_BYTES), &maps.m[T.bbuf], int32_t(T.b_row + k0), n0, full);
       }
-    if (xr)
-      for (int i = tid; i < BM * dim; i += NTH) {
-        int m = i / dim, q = i - m * dim;
-        sXr[m * XD + q] = (m0 + m < M) ? xr[size_t(m0 + m) * dim + q] : 0.0;
-      }
-  }
-
-  // producer cursor
-  int pt = grp.tbeg, pk = 0;
-  while (pt < grp.tend && terms[pt].K == 0) ++pt;
-
-  auto load_stage = [&](int stage) {
-    const Term T = terms[pt];
-    const int k0 = pk;
-    // B tile: BN columns x BK rows, 16-byte chunks along k
-    double* dB = sB + stage * S::B_STAGE;
-    for (int c = tid; c < BN * (BK / 2); c += NTH) {
-      int n = c / (BK / 2), kc = (c - n * (BK / 2)) * 2;
-      int gk = k0 + kc, gn = n0 + n;
-      bool v = (gn < R) && (gk < T.K);
-      const double* src = v ? T.b + gk + size_t(gn) * T.ldb : T.b;
-      cp_async16(dB + n * S::SB + kc, src, v);
-    }
-    double* dA = sA + stage * S::A_STAGE;
-    if (kGen && (T.flags & kTermGen)) {
-      if constexpr (kGen) {
-        double* dX = sXc + stage * BK * XD;
-        for (int i = tid; i < BK * dim; i += NTH) {
-          int kk = i / dim, q = i - kk * dim;
-          bool v = (k0 + kk) < T.K;
-          const double* src = v ? T.xc + size_t(k0 + kk) * dim + q : T.xc;
-          cp_async8(dX + kk * XD + q, src, v);
+      if (kGen && (T.flags & kTermGen)) {
+        if constexpr (kGen) {
+          const uint32_t dX = smem_u32(sX + stage * S::X_STAGE);
+          for (int i = pth; i < kBK * dim; i += kProducerThreads) {
+            const int kk = i / dim, q = i - kk * dim;
+            const bool v = (k0 + kk) < T.K;
+            cp_async8(dX + uint32_t(kk * XD + q) * 8u, v ? T.xc + size_t(k0 + kk) * dim + q : T.xc, v);
+          }
+        }
+      } else if (T.flags & kTermRowMajorA) {
+        // A[m][k] = a[k + m*lda]; 16-byte chunks along k
+        const uint32_t dA = smem_u32(sA + stage * S::A_STAGE);
+        const double* src0 = T.a + k0 + size_t(m0) * T.lda;
+#pragma unroll
+        for (int c = pth; c < BM * (kBK / 2); c += kProducerThreads) {
+          const int m = c >> 3, kc = (c & 7) * 2;
+          const bool v = (m0 + m < M) && (k0 + kc < T.K);
+          cp_async16(dA + uint32_t(m * S::SA_ROW + kc) * 8u, v ? src0 + kc + size_t(m) * T.lda : T.a, v);
+        }
+      } else {
+        // A[m][k] = a[m + k*lda]; 16-byte chunks along m
+        const uint32_t dA = smem_u32(sA + stage * S::A_STAGE);
+        const double* src0 = T.a + m0 + size_t(k0) * T.lda;
+#pragma unroll
+        for (int c = pth; c < kBK * (BM / 2); c += kProducerThreads) {
+          const int kk = c / (BM / 2), mc = (c % (BM / 2)) * 2;
+          const bool v = (m0 + mc < M) && (k0 + kk < T.K);
+          cp_async16(dA + uint32_t(kk * S::SA_COL + mc) * 8u, v ? src0 + mc + size_t(kk) * T.lda : T.a, v);
         }
       }
-    } else if (T.flags & kTermRowMajorA) {
-      for (int c = tid; c < BM * (BK / 2); c += NTH) {
-        int m = c / (BK / 2), kc = (c - m * (BK / 2)) * 2;
-        int gk = k0 + kc, gm = m0 + m;
-        bool v = (gm < M) && (gk < T.K);
-        const double* src = v ? T.a + gk + size_t(gm) * T.lda : T.a;
-        cp_async16(dA + m * S::SA_ROW + kc, src, v);
-      }
-    } else {
-      for (int c = tid; c < BK * (BM / 2); c += NTH) {
-        int kk = c / (BM / 2), mc = (c - kk * (BM / 2)) * 2;
-        int gk = k0 + kk, gm = m0 + mc;
-        bool v = (gm < M) && (gk < T.K);
-        const double* src = v ? T.a + gm + size_t(gk) * T.lda : T.a;
-        cp_async16(dA + kk * S::SA_COL + mc, src, v);
+      mbar_cp_async_arrive(full);
+      pk += kBK;
+      if (pk >= T.K) {
+        pk = 0;
+        ++pt;
+        while (pt < grp.tend && terms[pt].K == 0) ++pt;
       }
     }
-    // advance
-    pk += BK;
-    if (pk >= T.K) {
-      pk = 0;
-      ++pt;
-      while (pt < grp.tend && terms[pt].K == 0) ++pt;
+    asm volatile("cp.async.wait_all;\n" ::: "memory");  // never exit with copies in flight
+    return;
+  }
+
+  // =========================== CONSUMER WARPS ===========================
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kConsumerRegs));
+  const int cw = warp - kProducerThreads / 32;
+  const int g = lane >> 2, tig = lane & 3;
+  const int wm0 = (cw / WN) * S::WTM;
+  const int wn0 = (cw % WN) * S::WTN;
+
+  // row coordinates of generated terms (every generated term of a group shares its rows)
+  double xr[kGen ? S::MT : 1][kGen ? (DIM > 0 ? DIM : kMaxDimRt) : 1];
+  if constexpr (kGen) {
+    const double* xrp = nullptr;
+    for (int t = grp.tbeg; t < grp.tend; ++t)
+      if (terms[t].flags & kTermGen) {
+        xrp = terms[t].xr;
+        break;
+      }
+#pragma unroll
+    for (int i = 0; i < S::MT; ++i) {
+      const int m = m0 + wm0 + 8 * i + g;
+#pragma unroll
+      for (int q = 0; q < (DIM > 0 ? DIM : kMaxDimRt); ++q)
+        xr[i][q] = (xrp && m < M && q < dim) ? xrp[size_t(m) * dim + q] : 0.0;
     }
-  };
+  }
 
   double acc[S::MT][S::NT][2];
 #pragma unroll
@@ -309,64 +384,72 @@ __global__ void __launch_bounds__(WM* WN * 32)
 #pragma unroll
     for (int j = 0; j < S::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  // consumer cursor
+  // swizzled B fragment offsets: row n = wn0 + 8j + g has (n & 7) == g
+  uint32_t boff[kBK / 4];
+#pragma unroll
+  for (int ks = 0; ks < kBK / 4; ++ks) boff[ks] = swz128(wn0 + g, 4 * ks + tig);
+  const uint32_t sB_u = smem_u32(sB), sA_u = smem_u32(sA), sX_u = smem_u32(sX);
+
   int ct = grp.tbeg, ck = 0;
   while (ct < grp.tend && terms[ct].K == 0) ++ct;
-
-#pragma unroll 1
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < total) load_stage(s);
-    cp_async_commit();
-  }
-
 #pragma unroll 1
   for (int s = 0; s < total; ++s) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    if (s + STAGES - 1 < total) load_stage((s + STAGES - 1) % STAGES);
-    cp_async_commit();
-
     const int stage = s % STAGES;
     const int flags = terms[ct].flags;
     const int Kt = terms[ct].K;
-    const double* tA = sA + stage * S::A_STAGE;
-    const double* tB = sB + stage * S::B_STAGE;
-    const double* tX = sXc + stage * BK * XD;
+    mbar_wait(smem_u32(&bars[stage]), (s / STAGES) & 1);
+    const uint32_t tB = sB_u + stage * S::B_STAGE_BYTES;
+    const uint32_t tA = sA_u + stage * S::A_STAGE * 8;
+    const uint32_t tX = sX_u + stage * S::X_STAGE * 8;
+    // A fragments for the whole stage first: generated entries are 4*MT independent exp()
+    // chains per lane, so computing them together gives the FP64 pipe ILP instead of
+    // serialising one chain in front of every group of DMMAs
+    double a[kBK / 4][S::MT];
+    if (kGen && (flags & kTermGen)) {
+      if constexpr (kGen) {
 #pragma unroll
-    for (int ks = 0; ks < BK / 4; ++ks) {
-      const int kk = ks * 4 + tig;
-      double a[S::MT];
-      if (kGen && (flags & kTermGen)) {
-        if constexpr (kGen) {
+        for (int ks = 0; ks < kBK / 4; ++ks) {
+          const int kk = ks * 4 + tig;
           const bool kv = (ck + kk) < Kt;
+          double xc[DIM > 0 ? DIM : kMaxDimRt];
 #pragma unroll
-          for (int i = 0; i < S::MT; ++i) {
-            const int row = wm0 + 8 * i + g;
-            a[i] = kv ? kernel_entry<KIND, DIM>(sXr + row * XD, tX + kk * XD, kp) : 0.0;
-          }
+          for (int q = 0; q < (DIM > 0 ? DIM : kMaxDimRt); ++q)
+            if (DIM > 0 || q < dim) xc[q] = lds64(tX + uint32_t(kk * XD + q) * 8u);
+#pragma unroll
+          for (int i = 0; i < S::MT; ++i) a[ks][i] = kv ? kernel_entry<KIND, DIM>(xr[i], xc, kp) : 0.0;
         }
-      } else if (flags & kTermRowMajorA) {
-#pragma unroll
-        for (int i = 0; i < S::MT; ++i) a[i] = tA[(wm0 + 8 * i + g) * S::SA_ROW + kk];
-      } else {
-#pragma unroll
-        for (int i = 0; i < S::MT; ++i) a[i] = tA[kk * S::SA_COL + wm0 + 8 * i + g];
       }
+    } else if (flags & kTermRowMajorA) {
+#pragma unroll
+      for (int ks = 0; ks < kBK / 4; ++ks)
+#pragma unroll
+        for (int i = 0; i < S::MT; ++i)
+          a[ks][i] = lds64(tA + uint32_t((wm0 + 8 * i + g) * S::SA_ROW + ks * 4 + tig) * 8u);
+    } else {
+#pragma unroll
+      for (int ks = 0; ks < kBK / 4; ++ks)
+#pragma unroll
+        for (int i = 0; i < S::MT; ++i)
+          a[ks][i] = lds64(tA + uint32_t((ks * 4 + tig) * S::SA_COL + wm0 + 8 * i + g) * 8u);
+    }
+#pragma unroll
+    for (int ks = 0; ks < kBK / 4; ++ks) {
 #pragma unroll
       for (int j = 0; j < S::NT; ++j) {
-        const double b = tB[(wn0 + 8 * j + g) * S::SB + kk];
+        const double b = lds64(tB + boff[ks] + 1024u * j);
 #pragma unroll
-        for (int i = 0; i < S::MT; ++i) dmma884(acc[i][j][0], acc[i][j][1], a[i], b);
+        for (int i = 0; i < S::MT; ++i) dmma884(acc[i][j][0], acc[i][j][1], a[ks][i], b);
       }
     }
-    ck += BK;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&bars[STAGES + stage]));
+    ck += kBK;
     if (ck >= Kt) {
       ck = 0;
       ++ct;
       while (ct < grp.tend && terms[ct].K == 0) ++ct;
     }
   }
-  cp_async_wait<0>();
 
   // epilogue: registers -> C (column-major)
   double* c = cbase + grp.crow;
