@@ -7,14 +7,18 @@
 //     permute W (K5)  ->  N2S levels depth..1  ->  DOWNWARD levels 1..depth  ->  OUTPUT
 // Each launch is the grouped multi-term FP64 DMMA GEMM of gofmm_kernels.cuh.
 //
-// HBM layout (all FP64, column-major, every block start 16-byte aligned for cp.async):
-//   point space    : leaves left-to-right, leaf a at rows [pst_a, pst_a + pad2(n_a)); W_perm and
+// HBM layout (all FP64):
+//   point space    : leaves left-to-right, leaf a at rows [pst_a, pst_a + pad16(n_a)); W_perm and
 //                    the permuted coordinates live here (padding rows are zero)
 //   skeleton space : nodes in BFS id order (== level order), node a at rows
-//                    [soff_a, soff_a + pad2(k_a)); what (N2S output) and c (downward) live here.
+//                    [soff_a, soff_a + pad16(k_a)); what (N2S output) and c (downward) live here.
 //                    Siblings are adjacent, so [what_l; what_r] is one contiguous row range.
-//   proj_a         : k_a x ncand_pad column-major, ld = pad2(k_a); interior proj gets a zero
-//                    column after each odd-rank child so its columns line up with skeleton space.
+//   W_perm / what / c are stored in 16-ROW PANELS: panel p holds rows [16p, 16p+16) of all r_ws
+//                    columns contiguously (element (i, j) at (i/16)*16*r_ws + 16*j + i%16), so a
+//                    TMA box of 16 rows x BN columns is one contiguous 128*BN-byte run — a plain
+//                    column-major N x r layout would make every box touch BN 2 MB pages.
+//   proj_a         : k_a x ncand_pad column-major, ld = pad2(k_a); interior proj gets zero
+//                    columns so [child l; child r] candidates line up with skeleton space.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -49,6 +53,8 @@ struct Error : std::runtime_error {
   } while (0)
 
 inline int64_t pad2(int64_t x) { return (x + 1) & ~int64_t(1); }
+// point / skeleton space rows are padded to 16 so every node starts a 16-row panel (one TMA box)
+inline int64_t pad16(int64_t x) { return (x + 15) & ~int64_t(15); }
 
 struct DevBuf {
   void* p = nullptr;
@@ -87,12 +93,13 @@ struct DevBuf {
 //    8x256 — warps split M only, so every A entry is generated exactly once per CTA, and BN is
 //    wide to amortise exp() over the RHS columns.
 constexpr int kStages = 4, kBM_S = 128, kBN_S = 128, kBM_G = 64, kBN_G = 256;
-#define CFG_S kBM_S, kBN_S, 4, 2, kStages
-#define CFG_G kBM_G, kBN_G, 8, 1, kStages
-constexpr int kThreadsS = kProducerThreads + 4 * 2 * 32;
-constexpr int kThreadsG = kProducerThreads + 8 * 1 * 32;
+#define CFG_S kBM_S, kBN_S, 4, 4, kStages
+#define CFG_G kBM_G, kBN_G, 4, 4, kStages
+constexpr int kThreadsS = kProducerThreads + kConsumerThreads;
+constexpr int kThreadsG = kProducerThreads + kConsumerThreads;
 
-using KernelFn = void (*)(BMaps, const Tile*, const Group*, const Term*, int32_t, KernelParams, double*, int64_t);
+using KernelFn = void (*)(BMaps, const Tile*, const Group*, const Term*, int32_t, KernelParams, double*, int64_t,
+                          int32_t);
 
 struct GenKernel {
   KernelFn fn;
@@ -138,14 +145,15 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// B operand view of a column-major (ld x r) FP64 buffer: boxes of 16 rows x bn columns,
-// 128-byte swizzle (conflict-free fragment loads), out-of-range rows/columns read as zero.
-void encode_bmap(CUtensorMap* map, const double* ptr, int64_t ld, int32_t r, int bn) {
-  cuuint64_t dims[2] = {cuuint64_t(ld), cuuint64_t(r)};
-  cuuint64_t strides[1] = {cuuint64_t(ld) * sizeof(double)};
-  cuuint32_t box[2] = {cuuint32_t(kBK), cuuint32_t(bn)};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult rc = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims,
+// B operand view of a panel-layout FP64 buffer (rows x r used columns, r_ws allocated): a 3D
+// tensor {16 rows-in-panel, r columns, rows/16 panels}; boxes of 16 x bn x 1, 128-byte swizzle
+// (conflict-free fragment loads); columns >= r read as zero.
+void encode_bmap(CUtensorMap* map, const double* ptr, int64_t rows, int32_t r, int32_t r_ws, int bn) {
+  cuuint64_t dims[3] = {16, cuuint64_t(r), cuuint64_t(rows / 16)};
+  cuuint64_t strides[2] = {16 * sizeof(double), cuuint64_t(r_ws) * 16 * sizeof(double)};
+  cuuint32_t box[3] = {16, cuuint32_t(bn), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult rc = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ptr), dims,
                                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (rc != CUDA_SUCCESS) throw Error(GOFMM_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(rc)));
@@ -354,18 +362,18 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   int64_t off = 0;
   for (int id : H->leaf_ids) {
     H->pst[id] = off;
-    off += pad2(H->end[id] - H->start[id]);
+    off += pad16(H->end[id] - H->start[id]);
   }
-  H->ld_wp = std::max<int64_t>(pad2(off), 2);
+  H->ld_wp = std::max<int64_t>(pad16(off), 16);
   // skeleton space (BFS id order)
   H->soff.assign(nn, -1);
   off = 0;
   for (int i = 0; i < nn; ++i) {
     if (H->rank[i] < 0) continue;
     H->soff[i] = off;
-    off += pad2(H->rank[i]);
+    off += pad16(H->rank[i]);
   }
-  H->ld_s = std::max<int64_t>(pad2(off), 2);
+  H->ld_s = std::max<int64_t>(pad16(off), 16);
 
   // row map for the permutation kernel, and iperm
   std::vector<int32_t> prow(H->ld_wp, -1);
@@ -392,11 +400,11 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
           for (int r = 0; r < k; ++r) dst[r + j * ld] = src[r + int64_t(j) * k];
       } else {
         const int kl = H->rank[H->left[i]], kr = H->rank[H->right[i]];
-        const int64_t cpad = pad2(kl) + pad2(kr);
+        const int64_t cpad = pad16(kl) + pad16(kr);
         blob.resize(blob.size() + ld * cpad, 0.0);
         double* dst = blob.data() + H->proj_off[i];
         for (int j = 0; j < kl + kr; ++j) {
-          const int64_t jj = (j < kl) ? j : pad2(kl) + (j - kl);
+          const int64_t jj = (j < kl) ? j : pad16(kl) + (j - kl);
           for (int r = 0; r < k; ++r) dst[r + jj * ld] = src[r + int64_t(j) * k];
         }
       }
@@ -567,7 +575,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
       } else {
         t.b_buf = Buf::What;
         t.b_row = H->soff[H->left[i]];
-        t.K = int(pad2(H->rank[H->left[i]]) + pad2(H->rank[H->right[i]]));
+        t.K = int(pad16(H->rank[H->left[i]]) + pad16(H->rank[H->right[i]]));
       }
       flops += 2LL * H->rank[i] * ncand[i];
       H->phase_flops_per_rhs[0] += 2LL * H->rank[i] * ncand[i];
@@ -614,7 +622,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
         t.kind = 0;
         t.row_major = true;  // proj_p[:, off:off+k]^T
         t.a_blob = 0;
-        const int64_t coloff = (i == H->left[par]) ? 0 : pad2(H->rank[H->left[par]]);
+        const int64_t coloff = (i == H->left[par]) ? 0 : pad16(H->rank[H->left[par]]);
         t.lda = pad2(H->rank[par]);
         t.a_off = H->proj_off[par] + coloff * t.lda;
         t.b_buf = Buf::C;
@@ -800,10 +808,10 @@ void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double*
   if (H->maps_r != r) {
     // B operand tensor maps over the workspace buffers for this column count
     const double* bufs[3] = {H->d_wp.as<double>(), H->d_what.as<double>(), H->d_c.as<double>()};
-    const int64_t lds[3] = {H->ld_wp, H->ld_s, H->ld_s};
+    const int64_t rows[3] = {H->ld_wp, H->ld_s, H->ld_s};
     for (int b = 0; b < 3; ++b) {
-      encode_bmap(&H->maps_s.m[b], bufs[b], lds[b], r, kBN_S);
-      encode_bmap(&H->maps_g.m[b], bufs[b], lds[b], r, kBN_G);
+      encode_bmap(&H->maps_s.m[b], bufs[b], rows[b], r, H->ws_r, kBN_S);
+      encode_bmap(&H->maps_g.m[b], bufs[b], rows[b], r, H->ws_r, kBN_G);
     }
     H->maps_r = r;
   }
@@ -813,7 +821,7 @@ void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double*
     const int cpb = 8;  // columns per block: keeps the gathered source columns L2-resident
     dim3 grid(unsigned((H->ld_wp + 255) / 256), unsigned((r + cpb - 1) / cpb));
     permute_rows_in<<<grid, 256, 0, st>>>(d_w, ldw, H->d_prow.as<int32_t>(), H->ld_wp, r, cpb,
-                                          H->d_wp.as<double>(), H->ld_wp);
+                                          H->d_wp.as<double>(), int64_t(H->ws_r) * 16);
   }
   // ev[1 + p] marks the start of phase p (0 upward, 1 downward, 2 output); ev[4] the end
   if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[1], st));
@@ -822,20 +830,21 @@ void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double*
     while (timed && marked <= L.phase) GOFMM_CUDA(cudaEventRecord(H->ev[1 + marked++], st));
     double* cbase;
     int64_t ldc;
+    int32_t cpanel = 1;  // what / c: panel layout with panel stride 16*r_ws
     switch (L.out) {
-      case Buf::What: cbase = H->d_what.as<double>(); ldc = H->ld_s; break;
-      case Buf::C: cbase = H->d_c.as<double>(); ldc = H->ld_s; break;
-      default: cbase = d_u; ldc = ldu; break;
+      case Buf::What: cbase = H->d_what.as<double>(); ldc = int64_t(H->ws_r) * 16; break;
+      case Buf::C: cbase = H->d_c.as<double>(); ldc = int64_t(H->ws_r) * 16; break;
+      default: cbase = d_u; ldc = ldu; cpanel = 0; break;  // u_perm: caller's column-major buffer
     }
     const Tile* tiles = H->d_tiles.as<Tile>() + L.first_tile;
     if (L.gen) {
       dim3 grid(unsigned(L.ntiles), unsigned((r + kBN_G - 1) / kBN_G));
       H->kfn_g<<<grid, kThreadsG, H->smem_g, st>>>(H->maps_g, tiles, H->d_groups.as<Group>(), H->d_terms.as<Term>(),
-                                                    r, H->kp, cbase, ldc);
+                                                    r, H->kp, cbase, ldc, cpanel);
     } else {
       dim3 grid(unsigned(L.ntiles), unsigned((r + kBN_S - 1) / kBN_S));
       H->kfn_s<<<grid, kThreadsS, H->smem_s, st>>>(H->maps_s, tiles, H->d_groups.as<Group>(), H->d_terms.as<Term>(),
-                                                    r, H->kp, cbase, ldc);
+                                                    r, H->kp, cbase, ldc, cpanel);
     }
   }
   if (timed) {

@@ -131,6 +131,61 @@ __device__ __forceinline__ double eigen_redux_rt(const double* v, int n) {
 
 constexpr int kMaxDimRt = 16;
 
+__device__ __forceinline__ double lds64(uint32_t addr);
+template <int KIND, int DIM>
+__device__ __forceinline__ double kernel_entry(const double* xi, const double* xj, const KernelParams& kp);
+
+// exp(x) for x <= 0 (Gaussian / Matern arguments), |relative error| <= ~3 ulp:
+// x = (n/32) ln2 + f, |f| <= ln2/64, exp(f) by a degree-6 polynomial, 2^(j/32) from a 32-entry
+// shared-memory table, 2^(n>>5) by an exponent add. 11 FP64 pipe ops instead of the ~22 of the
+// libdevice exp; matrix-free entries are generated once per 256 output columns, so this is the
+// generation cost that competes with the DMMA pipe.
+__device__ __forceinline__ double exp_nonpos(double x, uint32_t tab) {
+  const double kInvL = 46.166241308446828384;                       // 32 / ln2
+  const double kShift = 6755399441055744.0;                         // 1.5 * 2^52
+  const double kLhi = 6.93147180369123816490e-01 / 32.0;            // fdlibm ln2_hi / 32
+  const double kLlo = 1.90821492927058770002e-10 / 32.0;            // fdlibm ln2_lo / 32
+  const double t = fma(x, kInvL, kShift);
+  const int n = __double2loint(t);
+  const double nd = t - kShift;
+  double f = fma(nd, -kLhi, x);
+  f = fma(nd, -kLlo, f);
+  double p = 1.0 / 720.0;
+  p = fma(p, f, 1.0 / 120.0);
+  p = fma(p, f, 1.0 / 24.0);
+  p = fma(p, f, 1.0 / 6.0);
+  p = fma(p, f, 0.5);
+  p = fma(p, f, 1.0);
+  p = fma(p, f, 1.0);
+  const double r = p * lds64(tab + uint32_t(n & 31) * 8u);
+  const int hi = __double2hiint(r) + ((n >> 5) << 20);
+  const double s = __hiloint2double(hi, __double2loint(r));
+  return x < -708.0 ? 0.0 : s;  // below ~2^-1022 the exponent add would wrap; K entries that small vanish
+}
+
+// K(x_i, x_j) as the reference generators build it (oracle.hpp:148-218): distance from the
+// difference vector, then the kernel function. d^2 is accumulated with FMAs (<= 1 ulp from the
+// reference's Eigen reduction); tab != 0 selects the table exp for Gaussian / Matern kernels.
+template <int KIND, int DIM>
+__device__ __forceinline__ double kernel_entry_fast(const double* xi, const double* xj, const KernelParams& kp,
+                                                    uint32_t tab) {
+  if constexpr ((KIND == kGaussian || KIND == kExponential) && DIM > 0) {
+    double d2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < DIM; ++q) {
+      const double e = xi[q] - xj[q];
+      d2 = (q == 0) ? e * e : fma(e, e, d2);
+    }
+    if constexpr (KIND == kGaussian) {
+      return exp_nonpos(-d2 * kp.p0, tab);
+    } else {
+      return exp_nonpos(-sqrt(d2) * kp.p0, tab);
+    }
+  } else {
+    return kernel_entry<KIND, DIM>(xi, xj, kp);
+  }
+}
+
 // K(x_i, x_j) exactly as the reference generators build it (oracle.hpp:148-218).
 template <int KIND, int DIM>
 __device__ __forceinline__ double kernel_entry(const double* xi, const double* xj, const KernelParams& kp) {
@@ -201,12 +256,12 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
-                                            uint32_t bar) {
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            int32_t c2, uint32_t bar) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-      "[%4];\n" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
 }
 
@@ -221,30 +276,38 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 // ------------------------------------------------------------------ grouped multi-term GEMM
 constexpr int kBK = 16;  // k-depth per stage: one 128-byte TMA row of FP64
 
-// Warp roles: warpgroup 0 = producer (4 warps; lane 0 of warp 0 issues TMA, all 128 threads
-// stage cp.async operands), warpgroups 1..2 = 8 consumer warps. setmaxnreg moves registers from
-// the producer (56) to the consumers (224): with 12 resident warps (3 per SM sub-partition) the
-// launch budget is 168 per thread, too few for 64 FP64 accumulators without spills.
+// Warp roles: warpgroup 0 = producer (4 warps: thread 0 issues the B-tile TMA, all 128 threads
+// stage stored A tiles / point coordinates with cp.async), then 16 consumer warps (4 per SM
+// sub-partition, enough to keep the DMMA pipe fed through LDS and exp() latencies).
+// setmaxnreg moves registers from the producer to the consumers: 640 threads launch with
+// kLaunchRegs each; the producer drops to kProducerRegs, the consumers rise to kConsumerRegs.
 constexpr int kProducerThreads = 128;
-constexpr int kProducerRegs = 56, kConsumerRegs = 224;
+constexpr int kConsumerWarps = 16;
+constexpr int kConsumerThreads = kConsumerWarps * 32;
+constexpr int kLaunchRegs = 96, kProducerRegs = 56, kConsumerRegs = 104;
+// setmaxnreg.inc blocks until the registers exist: the producer must release what consumers add
+static_assert(4 * (kLaunchRegs - kProducerRegs) >= kConsumerWarps * (kConsumerRegs - kLaunchRegs),
+              "setmaxnreg balance");
 
 template <int BM, int BN, int WM, int WN, int STAGES, int XD>
 struct GemmShape {
-  static constexpr int kConsumers = WM * WN;
-  static_assert(kConsumers == 8, "two consumer warpgroups");
-  static constexpr int kThreads = kProducerThreads + kConsumers * 32;
+  static_assert(WM * WN == kConsumerWarps, "consumer warp grid");
+  static constexpr int kThreads = kProducerThreads + kConsumerThreads;
   static constexpr int WTM = BM / WM, WTN = BN / WN;
   static constexpr int MT = WTM / 8, NT = WTN / 8;
-  static constexpr int SA_COL = BM + 4;   // stored A column-major tile [BK][BM+4] (m contiguous)
-  static constexpr int SA_ROW = kBK + 4;  // stored A row-major tile    [BM][BK+4] (k contiguous)
+  static constexpr int SA_COL = BM;       // stored A column-major tile [BK][BM], XOR-swizzled chunks
+  static constexpr int SA_ROW = kBK + 2;  // row-major / generated A tile [BM][BK+2]
   static constexpr int A_STAGE = (kBK * SA_COL > BM * SA_ROW) ? kBK * SA_COL : BM * SA_ROW;  // doubles
   static constexpr int B_STAGE_BYTES = BN * kBK * 8;  // TMA box, 128B-swizzled rows, 1024B aligned
   static constexpr int X_STAGE = kBK * XD;            // column coordinates (generated terms)
+  static constexpr int GEN_PER_THREAD = (BM * kBK) / kConsumerThreads;
   static_assert(BM % (8 * WM) == 0 && BN % (8 * WN) == 0 && BN <= 256, "tile shape");
   static_assert(B_STAGE_BYTES % 1024 == 0, "swizzle-128B tiles need 1024-byte multiples");
-  static constexpr size_t smem_bytes =
-      1024 /* alignment slack */ + size_t(STAGES) * B_STAGE_BYTES + size_t(STAGES) * A_STAGE * 8 +
-      size_t(STAGES) * X_STAGE * 8 + size_t(2 * STAGES) * 8;
+  static_assert((BM * kBK) % kConsumerThreads == 0 && kConsumerThreads % BM == 0, "generation mapping");
+  static constexpr size_t smem_bytes = 1024 /* alignment slack */ + size_t(STAGES) * B_STAGE_BYTES +
+                                       size_t(STAGES) * A_STAGE * 8 + size_t(STAGES) * X_STAGE * 8 +
+                                       size_t(3 * STAGES) * 8 + 32 * 8 /* exp table */ +
+                                       size_t(BM) * XD * 8 /* row coordinates */;
 };
 
 template <int BM, int BN, int WM, int WN, int STAGES, int KIND, int DIM>
@@ -258,21 +321,42 @@ __device__ __forceinline__ uint32_t swz128(int n, int k) {
   return uint32_t(n) * 128u + ((uint32_t((k >> 1) ^ (n & 7)) << 4) | (uint32_t(k & 1) << 3));
 }
 
+// Physical k of MMA k-slot `tig` in sub-step `ks` of a 16-deep stage. The DMMA reduction is
+// order-free in k, so A and B may use any common permutation; this one makes every half-warp
+// of a 64-bit fragment load touch all 32 banks of the 128B-swizzled B tile (the identity map
+// leaves a 2-way conflict per half-warp).
+__device__ __forceinline__ int kpi(int ks, int tig) { return 2 * ks + (tig & 1) + 8 * (tig >> 1); }
+
+// Column-major stored A tile [BK][BM]: 16-byte chunk (2 consecutive m) index XORed with 2*h(k),
+// h distinct for the four k of one sub-step, so fragment loads are conflict-free as well.
+__device__ __forceinline__ int acol_chunk(int k, int mchunk) {
+  return mchunk ^ (2 * ((k & 1) | (((k >> 3) & 1) << 1)));
+}
+
+__device__ __forceinline__ void consumer_bar() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerThreads) : "memory");
+}
+
 template <int BM, int BN, int WM, int WN, int STAGES, int KIND, int DIM>
-__global__ void __launch_bounds__(kProducerThreads + WM * WN * 32, 1)
+__global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
     grouped_gemm_f64(const __grid_constant__ BMaps maps, const Tile* __restrict__ tiles,
                      const Group* __restrict__ groups, const Term* __restrict__ terms, int32_t R, KernelParams kp,
-                     double* __restrict__ cbase, int64_t ldc) {
+                     double* __restrict__ cbase, int64_t ldc, int32_t cpanel) {
   constexpr bool kGen = (KIND != kKindNone);
   constexpr int XD = kGen ? (DIM > 0 ? DIM + 1 : kMaxDimRt + 1) : 0;  // odd stride: no bank conflicts
+  constexpr int DD = DIM > 0 ? DIM : kMaxDimRt;
   using S = GemmShape<BM, BN, WM, WN, STAGES, XD>;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* sB = base;                                                  // [STAGES][BN*128B]
   double* sA = reinterpret_cast<double*>(sB + STAGES * S::B_STAGE_BYTES);    // [STAGES][A_STAGE]
   double* sX = sA + STAGES * S::A_STAGE;                                     // [STAGES][BK][XD]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sX + STAGES * S::X_STAGE);    // full[STAGES], empty[STAGES]
+  // full[STAGES] (producer -> consumers), empty[STAGES] (consumers -> producer),
+  // gen[STAGES] (consumers -> consumers: generated A tile of the stage is complete)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sX + STAGES * S::X_STAGE);
+  double* sTab = reinterpret_cast<double*>(bars + 3 * STAGES);               // 2^(j/32), j < 32
+  double* sXr = sTab + 32;                                                   // [BM][XD] row coordinates
 
   const Tile tile = tiles[blockIdx.x];
   const Group grp = groups[tile.group];
@@ -284,11 +368,13 @@ __global__ void __launch_bounds__(kProducerThreads + WM * WN * 32, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(smem_u32(&bars[s]), kProducerThreads + 1);  // producer cp.async arrivals + 1 expect_tx
-      mbar_init(smem_u32(&bars[STAGES + s]), S::kConsumers);
+      mbar_init(smem_u32(&bars[s]), kProducerThreads + 1);  // producer arrivals + 1 expect_tx
+      mbar_init(smem_u32(&bars[STAGES + s]), kConsumerWarps);
+      mbar_init(smem_u32(&bars[2 * STAGES + s]), kConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  if (threadIdx.x < 32) sTab[threadIdx.x] = exp2(double(threadIdx.x) * (1.0 / 32.0));
   __syncthreads();
 
   // total pipeline steps across all terms
@@ -309,7 +395,9 @@ __global__ void __launch_bounds__(kProducerThreads + WM * WN * 32, 1)
       const int k0 = pk;
       if (pth == 0) {
         mbar_arrive_expect_tx(full, S::B_STAGE_BYTES);
-        tma_load_2d(smem_u32(sB + stage * S::B_STAGE_BYTES), &maps.m[T.bbuf], int32_t(T.b_row + k0), n0, full);
+        // B rows [b_row + k0, +16) = one 16-row panel (b_row is 16-aligned): a contiguous run
+        tma_load_3d(smem_u32(sB + stage * S::B_STAGE_BYTES), &maps.m[T.bbuf], 0, n0,
+                    int32_t((T.b_row + k0) >> 4), full);
       }
       if (kGen && (T.flags & kTermGen)) {
         if constexpr (kGen) {
@@ -324,21 +412,22 @@ __global__ void __launch_bounds__(kProducerThreads + WM * WN * 32, 1)
         // A[m][k] = a[k + m*lda]; 16-byte chunks along k
         const uint32_t dA = smem_u32(sA + stage * S::A_STAGE);
         const double* src0 = T.a + k0 + size_t(m0) * T.lda;
-#pragma unroll
+#pragma unroll 2
         for (int c = pth; c < BM * (kBK / 2); c += kProducerThreads) {
           const int m = c >> 3, kc = (c & 7) * 2;
           const bool v = (m0 + m < M) && (k0 + kc < T.K);
           cp_async16(dA + uint32_t(m * S::SA_ROW + kc) * 8u, v ? src0 + kc + size_t(m) * T.lda : T.a, v);
         }
       } else {
-        // A[m][k] = a[m + k*lda]; 16-byte chunks along m
+        // A[m][k] = a[m + k*lda]; 16-byte chunks along m, chunk index swizzled per k row
         const uint32_t dA = smem_u32(sA + stage * S::A_STAGE);
         const double* src0 = T.a + m0 + size_t(k0) * T.lda;
-#pragma unroll
+#pragma unroll 2
         for (int c = pth; c < kBK * (BM / 2); c += kProducerThreads) {
-          const int kk = c / (BM / 2), mc = (c % (BM / 2)) * 2;
+          const int kk = c / (BM / 2), mch = c % (BM / 2), mc = mch * 2;
           const bool v = (m0 + mc < M) && (k0 + kk < T.K);
-          cp_async16(dA + uint32_t(kk * S::SA_COL + mc) * 8u, v ? src0 + mc + size_t(kk) * T.lda : T.a, v);
+          cp_async16(dA + uint32_t(kk * S::SA_COL + 2 * acol_chunk(kk, mch)) * 8u,
+                     v ? src0 + mc + size_t(kk) * T.lda : T.a, v);
         }
       }
       mbar_cp_async_arrive(full);
@@ -355,28 +444,56 @@ __global__ void __launch_bounds__(kProducerThreads + WM * WN * 32, 1)
 
   // =========================== CONSUMER WARPS ===========================
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kConsumerRegs));
-  const int cw = warp - kProducerThreads / 32;
+  const int cth = threadIdx.x - kProducerThreads;
+  const int cw = cth >> 5;
   const int g = lane >> 2, tig = lane & 3;
   const int wm0 = (cw / WN) * S::WTM;
   const int wn0 = (cw % WN) * S::WTN;
+  const uint32_t sB_u = smem_u32(sB), sA_u = smem_u32(sA), sX_u = smem_u32(sX);
+  const uint32_t tabU = smem_u32(sTab);
 
-  // row coordinates of generated terms (every generated term of a group shares its rows)
-  double xr[kGen ? S::MT : 1][kGen ? (DIM > 0 ? DIM : kMaxDimRt) : 1];
+  // generated terms: this thread produces rows gen_m, columns gen_k + i*(threads/BM) of each
+  // BM x 16 tile, cooperatively with the other consumers (each entry is computed once per CTA)
+  const int gen_m = cth % BM, gen_k = cth / BM;
   if constexpr (kGen) {
+    // rows of every generated term of a group are the group's own points: stage them once
     const double* xrp = nullptr;
     for (int t = grp.tbeg; t < grp.tend; ++t)
       if (terms[t].flags & kTermGen) {
         xrp = terms[t].xr;
         break;
       }
-#pragma unroll
-    for (int i = 0; i < S::MT; ++i) {
-      const int m = m0 + wm0 + 8 * i + g;
-#pragma unroll
-      for (int q = 0; q < (DIM > 0 ? DIM : kMaxDimRt); ++q)
-        xr[i][q] = (xrp && m < M && q < dim) ? xrp[size_t(m) * dim + q] : 0.0;
-    }
+    if (xrp)
+      for (int i = cth; i < BM * dim; i += kConsumerThreads) {
+        const int m = i / dim, q = i - m * dim;
+        sXr[m * XD + q] = (m0 + m < M) ? xrp[size_t(m0 + m) * dim + q] : 0.0;
+      }
+    consumer_bar();
   }
+  const uint32_t xrU = smem_u32(sXr) + uint32_t(gen_m * XD) * 8u;
+  // fill the row-major A tile of stage s from the column coordinates the producer staged
+  auto generate = [&](int s, int k0, int Kt) {
+    if constexpr (kGen) {
+      const int stage = s % STAGES;
+      const uint32_t tX = sX_u + stage * S::X_STAGE * 8;
+      const uint32_t tA = sA_u + stage * S::A_STAGE * 8;
+      const bool row_ok = m0 + gen_m < M;
+#pragma unroll
+      for (int i = 0; i < S::GEN_PER_THREAD; ++i) {
+        const int kk = gen_k + i * (kConsumerThreads / BM);
+        double xc[DD], xr[DD];
+#pragma unroll
+        for (int q = 0; q < DD; ++q)
+          if (DIM > 0 || q < dim) {
+            xc[q] = lds64(tX + uint32_t(kk * XD + q) * 8u);
+            xr[q] = lds64(xrU + uint32_t(q) * 8u);
+          }
+        const double v = (row_ok && k0 + kk < Kt) ? kernel_entry_fast<KIND, DIM>(xr, xc, kp, tabU) : 0.0;
+        asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(tA + uint32_t(gen_m * S::SA_ROW + kk) * 8u), "d"(v)
+                     : "memory");
+      }
+    }
+  };
 
   double acc[S::MT][S::NT][2];
 #pragma unroll
@@ -387,96 +504,93 @@ __global__ void __launch_bounds__(kProducerThreads + WM * WN * 32, 1)
   // swizzled B fragment offsets: row n = wn0 + 8j + g has (n & 7) == g
   uint32_t boff[kBK / 4];
 #pragma unroll
-  for (int ks = 0; ks < kBK / 4; ++ks) boff[ks] = swz128(wn0 + g, 4 * ks + tig);
-  const uint32_t sB_u = smem_u32(sB), sA_u = smem_u32(sA), sX_u = smem_u32(sX);
+  for (int ks = 0; ks < kBK / 4; ++ks) boff[ks] = swz128(wn0 + g, kpi(ks, tig));
 
+  auto advance = [&](int& t, int& k) {
+    k += kBK;
+    if (k >= terms[t].K) {
+      k = 0;
+      ++t;
+      while (t < grp.tend && terms[t].K == 0) ++t;
+    }
+  };
   int ct = grp.tbeg, ck = 0;
   while (ct < grp.tend && terms[ct].K == 0) ++ct;
+  // Stage s+1 is waited for (and, if generated, generated) while stage s is multiplied; a
+  // generated tile is published through the stage's `gen` mbarrier (one arrival per consumer
+  // warp), so warps only wait for each other when one falls a whole stage behind.
+  auto stage_in = [&](int s, int t, int k) {
+    mbar_wait(smem_u32(&bars[s % STAGES]), (s / STAGES) & 1);
+    if constexpr (kGen) {
+      if (terms[t].flags & kTermGen) generate(s, k, terms[t].K);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bars[2 * STAGES + s % STAGES]));
+    }
+  };
+  if (total > 0) stage_in(0, ct, ck);
 #pragma unroll 1
   for (int s = 0; s < total; ++s) {
     const int stage = s % STAGES;
     const int flags = terms[ct].flags;
-    const int Kt = terms[ct].K;
-    mbar_wait(smem_u32(&bars[stage]), (s / STAGES) & 1);
-    const uint32_t tB = sB_u + stage * S::B_STAGE_BYTES;
+    int nt = ct, nk = ck;
+    advance(nt, nk);
+    if (s + 1 < total) stage_in(s + 1, nt, nk);
+    if constexpr (kGen) mbar_wait(smem_u32(&bars[2 * STAGES + stage]), (s / STAGES) & 1);
+    const bool rowA = (flags & (kTermRowMajorA | kTermGen)) != 0;  // generated tiles are row-major
     const uint32_t tA = sA_u + stage * S::A_STAGE * 8;
-    const uint32_t tX = sX_u + stage * S::X_STAGE * 8;
-    // A fragments for the whole stage first: generated entries are 4*MT independent exp()
-    // chains per lane, so computing them together gives the FP64 pipe ILP instead of
-    // serialising one chain in front of every group of DMMAs
-    double a[kBK / 4][S::MT];
-    if (kGen && (flags & kTermGen)) {
-      if constexpr (kGen) {
-#pragma unroll
-        for (int ks = 0; ks < kBK / 4; ++ks) {
-          const int kk = ks * 4 + tig;
-          const bool kv = (ck + kk) < Kt;
-          double xc[DIM > 0 ? DIM : kMaxDimRt];
-#pragma unroll
-          for (int q = 0; q < (DIM > 0 ? DIM : kMaxDimRt); ++q)
-            if (DIM > 0 || q < dim) xc[q] = lds64(tX + uint32_t(kk * XD + q) * 8u);
-#pragma unroll
-          for (int i = 0; i < S::MT; ++i) a[ks][i] = kv ? kernel_entry<KIND, DIM>(xr[i], xc, kp) : 0.0;
-        }
-      }
-    } else if (flags & kTermRowMajorA) {
-#pragma unroll
-      for (int ks = 0; ks < kBK / 4; ++ks)
-#pragma unroll
-        for (int i = 0; i < S::MT; ++i)
-          a[ks][i] = lds64(tA + uint32_t((wm0 + 8 * i + g) * S::SA_ROW + ks * 4 + tig) * 8u);
-    } else {
-#pragma unroll
-      for (int ks = 0; ks < kBK / 4; ++ks)
-#pragma unroll
-        for (int i = 0; i < S::MT; ++i)
-          a[ks][i] = lds64(tA + uint32_t((ks * 4 + tig) * S::SA_COL + wm0 + 8 * i + g) * 8u);
-    }
+    const uint32_t tB = sB_u + stage * S::B_STAGE_BYTES;
 #pragma unroll
     for (int ks = 0; ks < kBK / 4; ++ks) {
+      double a[S::MT];
+#pragma unroll
+      for (int i = 0; i < S::MT; ++i) {
+        const int kk = kpi(ks, tig), m = wm0 + 8 * i + g;
+        a[i] = rowA ? lds64(tA + uint32_t(m * S::SA_ROW + kk) * 8u)
+                    : lds64(tA + uint32_t(kk * S::SA_COL + 2 * acol_chunk(kk, m >> 1) + (m & 1)) * 8u);
+      }
 #pragma unroll
       for (int j = 0; j < S::NT; ++j) {
         const double b = lds64(tB + boff[ks] + 1024u * j);
 #pragma unroll
-        for (int i = 0; i < S::MT; ++i) dmma884(acc[i][j][0], acc[i][j][1], a[ks][i], b);
+        for (int i = 0; i < S::MT; ++i) dmma884(acc[i][j][0], acc[i][j][1], a[i], b);
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&bars[STAGES + stage]));
-    ck += kBK;
-    if (ck >= Kt) {
-      ck = 0;
-      ++ct;
-      while (ct < grp.tend && terms[ct].K == 0) ++ct;
-    }
+    ct = nt;
+    ck = nk;
   }
 
-  // epilogue: registers -> C (column-major)
-  double* c = cbase + grp.crow;
+  // epilogue: registers -> C; what / c in 16-row panels (crow is 16-aligned), u_perm column-major
 #pragma unroll
   for (int i = 0; i < S::MT; ++i) {
     const int m = m0 + wm0 + 8 * i + g;
     if (m >= M) continue;
+    double* crow_ptr = cpanel ? cbase + (grp.crow >> 4) * ldc + size_t(m >> 4) * ldc + (m & 15)
+                              : cbase + grp.crow + m;
+    const size_t cstride = cpanel ? 16 : size_t(ldc);
 #pragma unroll
     for (int j = 0; j < S::NT; ++j) {
       const int n = n0 + wn0 + 8 * j + 2 * tig;
-      if (n < R) c[m + size_t(n) * ldc] = acc[i][j][0];
-      if (n + 1 < R) c[m + size_t(n + 1) * ldc] = acc[i][j][1];
+      if (n < R) crow_ptr[size_t(n) * cstride] = acc[i][j][0];
+      if (n + 1 < R) crow_ptr[size_t(n + 1) * cstride] = acc[i][j][1];
     }
   }
 }
 
 // ------------------------------------------------------------------ permutations (K5)
-// wp[t, c] = w[prow[t], c]   (evaluate.hpp:294-295, into the padded leaf layout; prow = -1 pads)
+// wp[t, c] = w[prow[t], c]   (evaluate.hpp:294-295) into the padded leaf layout, stored in
+// 16-row panels (panel stride `pstride` doubles); prow = -1 marks padding rows (written as 0)
 __global__ void permute_rows_in(const double* __restrict__ w, int64_t ldw, const int32_t* __restrict__ prow,
                                 int64_t npad, int32_t r, int32_t cols_per_block, double* __restrict__ wp,
-                                int64_t ldp) {
+                                int64_t pstride) {
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= npad) return;
   const int32_t src = prow[t];
   const int c0 = blockIdx.y * cols_per_block;
   const int c1 = min(r, c0 + cols_per_block);
-  for (int c = c0; c < c1; ++c) wp[t + size_t(c) * ldp] = (src >= 0) ? __ldg(w + src + size_t(c) * ldw) : 0.0;
+  double* dst = wp + (t >> 4) * pstride + (t & 15);
+  for (int c = c0; c < c1; ++c) dst[size_t(c) * 16] = (src >= 0) ? __ldg(w + src + size_t(c) * ldw) : 0.0;
 }
 
 // u[iperm[t], c] = up[t, c]   (unpermute, evaluate.hpp:21-25)
