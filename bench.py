@@ -235,21 +235,26 @@ def ours_arm(args, world, rank, local):
     ms = allmax(ms, world)
     value = world * flops / (ms * 1e-3) / 1e9  # whole-job GFLOP/s
 
-    # per-phase device times of one more evaluation (CUDA events on the launch stream)
+    # per-phase and per-launch device times of one more evaluation (CUDA events on the stream the
+    # kernels are launched on); the roofline reports the longest single launch
     _, ph = ev.evaluate_torch(w, out=u, sync_stats=True)
     torch.cuda.synchronize()
     peak, peak_src = fp64_peak_tflops()
     phases = {"upward": (pflops["upward"], ph["ms_upward"]), "downward": (pflops["downward"], ph["ms_downward"]),
               "output": (pflops["output"], ph["ms_output"])}
-    dom = max(phases, key=lambda k: phases[k][1])
-    dflops, dms = phases[dom]
-    achieved = dflops / (dms * 1e-3) / 1e12 if dms > 0 else 0.0
+    launches = ev.launch_profile(r)
+    dom = max(launches, key=lambda x: x["ms"])
+    achieved = dom["flops"] / (dom["ms"] * 1e-3) / 1e12 if dom["ms"] > 0 else 0.0
+    dom_name = f"grouped_gemm_f64 {dom['phase']} launch (level {dom['level']})" if dom["level"] >= 0 else \
+        "grouped_gemm_f64 output launch (L2L + leaf S2N)"
     traffic = None
     try:
         with open(NCU_SUMMARY_FILE) as f:
             nsum = json.load(f)
-        if nsum.get("config") == args.config and nsum.get("phase") == dom:
-            traffic = nsum.get("dram_bytes_per_launch")
+        for rec in nsum.get("launches", []):
+            if (rec.get("config") == args.config and rec.get("phase") == dom["phase"]
+                    and rec.get("level") == dom["level"] and rec.get("n") == tree.n and rec.get("r") == r):
+                traffic = rec.get("dram_bytes")
     except Exception:
         pass
 
@@ -312,9 +317,10 @@ def ours_arm(args, world, rank, local):
         "flops_per_eval": int(flops),
         "rel_error": rel_err,
         "phase_ms": {k: round(v[1], 3) for k, v in phases.items()} | {"permute": round(ph["ms_permute"], 3)},
-        "roofline": {"bound": "tensor", "kernel": f"grouped_gemm_f64 ({dom} phase)", "achieved": round(achieved, 3),
+        "roofline": {"bound": "tensor", "kernel": dom_name, "achieved": round(achieved, 3),
                      "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "peak_source": peak_src},
+                     "peak_source": peak_src, "launch_ms": round(dom["ms"], 3), "launch_flops": int(dom["flops"]),
+                     "share_of_step": round(dom["ms"] / ms, 4)},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(ev.launches_per_eval * args.steps),

@@ -137,6 +137,22 @@ int64_t gofmm_flops(const gofmm_handle* h, int32_t r);
  * downward (S2S + S2N), output (L2L + leaf S2N)}. */
 int gofmm_phase_flops(const gofmm_handle* h, int32_t r, int64_t* out3);
 
+/* Per-launch breakdown of one evaluation (for roofline reporting): the plan's grouped-GEMM
+ * launches in issue order; ms is the CUDA-event duration from the last evaluation run with
+ * stats (gofmm_evaluate, or gofmm_evaluate_device with stats_sync), -1 if none yet. */
+typedef struct gofmm_launch_info {
+  int32_t phase;     /* 0 upward (N2S), 1 downward (S2S + S2N), 2 output (L2L + leaf S2N) */
+  int32_t level;     /* tree level (-1 for the output launch) */
+  int64_t ctas;      /* grid size for this r */
+  int64_t flops;     /* reference-counted flops of this launch for r columns */
+  double ms;         /* measured duration */
+  int32_t generated; /* 1 if the launch generates K entries from coordinates */
+  int32_t reserved;
+} gofmm_launch_info;
+
+/* Fill up to cap entries of `out`; *count receives the number of launches. */
+int gofmm_launch_profile(const gofmm_handle* h, int32_t r, int32_t cap, gofmm_launch_info* out, int32_t* count);
+
 /* Bytes of device memory held by the handle (tree + workspace). */
 int64_t gofmm_device_bytes(const gofmm_handle* h);
 

@@ -79,6 +79,11 @@ class EvalStats(C.Structure):
                 ("ms_h2d", C.c_double), ("ms_d2h", C.c_double)]
 
 
+class LaunchInfo(C.Structure):
+    _fields_ = [("phase", C.c_int32), ("level", C.c_int32), ("ctas", C.c_int64), ("flops", C.c_int64),
+                ("ms", C.c_double), ("generated", C.c_int32), ("reserved", C.c_int32)]
+
+
 class GofmmError(RuntimeError):
     """Raised for non-zero C-ABI return codes; ``code`` follows gfmm_cli.cpp:289-305."""
 
@@ -95,7 +100,7 @@ _lib = None
 
 # every symbol include/gofmm_b200.h declares
 EXPORTS = ("gofmm_create", "gofmm_evaluate", "gofmm_evaluate_device", "gofmm_unpermute_device",
-           "gofmm_flops", "gofmm_phase_flops", "gofmm_device_bytes", "gofmm_launches_per_eval", "gofmm_destroy",
+           "gofmm_flops", "gofmm_phase_flops", "gofmm_launch_profile", "gofmm_device_bytes", "gofmm_launches_per_eval", "gofmm_destroy",
            "gofmm_last_error", "gofmm_abi_version")
 
 
@@ -114,6 +119,7 @@ def lib():
         L.gofmm_flops.argtypes = [P, C.c_int32]
         L.gofmm_flops.restype = C.c_int64
         L.gofmm_phase_flops.argtypes = [P, C.c_int32, P]
+        L.gofmm_launch_profile.argtypes = [P, C.c_int32, C.c_int32, P, C.POINTER(C.c_int32)]
         L.gofmm_device_bytes.argtypes = [P]
         L.gofmm_device_bytes.restype = C.c_int64
         L.gofmm_launches_per_eval.argtypes = [P]

@@ -92,9 +92,9 @@ struct DevBuf {
 // G: generated-operand GEMMs (matrix-free L2L and S2S): 64x256 CTA tile, 8 consumer warps of
 //    8x256 — warps split M only, so every A entry is generated exactly once per CTA, and BN is
 //    wide to amortise exp() over the RHS columns.
-constexpr int kStages = 4, kBM_S = 128, kBN_S = 128, kBM_G = 64, kBN_G = 256;
-#define CFG_S kBM_S, kBN_S, 4, 4, kStages
-#define CFG_G kBM_G, kBN_G, 4, 4, kStages
+constexpr int kStagesS = 5, kStagesG = 5, kBM_S = 128, kBN_S = 128, kBM_G = 64, kBN_G = 256;
+#define CFG_S kBM_S, kBN_S, 4, 4, kStagesS
+#define CFG_G kBM_G, kBN_G, 4, 4, kStagesG
 constexpr int kThreadsS = kProducerThreads + kConsumerThreads;
 constexpr int kThreadsG = kProducerThreads + kConsumerThreads;
 
@@ -212,6 +212,8 @@ struct Launch {
   bool gen = false;  // G config (generated operands present)
   Buf out;
   int phase;  // 0 upward, 1 downward, 2 output
+  int level;  // tree level (output launch: -1)
+  int64_t flops_per_rhs = 0;  // reference-counted flops of this launch per RHS column
 };
 
 }  // namespace
@@ -221,6 +223,8 @@ struct gofmm_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
+  std::vector<cudaEvent_t> lev;  // per-launch start/stop events (timed evaluations only)
+  std::vector<float> launch_ms;  // durations of the last timed evaluation
   int32_t n = 0, num_nodes = 0, depth = 0, dim = 0, kernel = -1, source = 0;
   gofmm::KernelParams kp{};
   int near_mode = GOFMM_BLOCKS_MATRIX_FREE, far_mode = GOFMM_BLOCKS_MATRIX_FREE;
@@ -538,12 +542,16 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   const bool gen_near = !stored && !mat_near;
   const bool gen_far = !stored && !mat_far;
   int64_t flops = 0;
-  auto push_launch = [&](std::vector<HostGroup>& gs, bool gen, Buf out, int phase) {
+  int64_t flops_mark = 0;
+  auto push_launch = [&](std::vector<HostGroup>& gs, bool gen, Buf out, int phase, int level) {
     Launch L;
     L.first_tile = int(H->tiles.size());
     L.gen = gen;
     L.out = out;
     L.phase = phase;
+    L.level = level;
+    L.flops_per_rhs = flops - flops_mark;
+    flops_mark = flops;
     const int BM = gen ? kBM_G : kBM_S;
     for (auto& g : gs) {
       const int gid = int(H->groups.size());
@@ -582,7 +590,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
       g.terms.push_back(t);
       gs.push_back(std::move(g));
     }
-    push_launch(gs, false, Buf::What, 0);
+    push_launch(gs, false, Buf::What, 0, lev);
   }
 
   // downward: coupling (S2S) + parent term (S2N), top level first (evaluate.hpp:95-111,164-195)
@@ -634,7 +642,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
       }
       gs.push_back(std::move(g));
     }
-    push_launch(gs, any_gen, Buf::C, 1);
+    push_launch(gs, any_gen, Buf::C, 1, lev);
   }
 
   // output: D, near blocks (ascending index), proj^T c (evaluate.hpp:113-117,196-217)
@@ -699,7 +707,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
       }
       gs.push_back(std::move(g));
     }
-    push_launch(gs, gen_near, Buf::Out, 2);
+    push_launch(gs, gen_near, Buf::Out, 2, -1);
   }
   H->flops_per_rhs = flops;
   H->phase_flops_per_rhs[2] = flops - H->phase_flops_per_rhs[0] - H->phase_flops_per_rhs[1];
@@ -837,6 +845,8 @@ void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double*
       default: cbase = d_u; ldc = ldu; cpanel = 0; break;  // u_perm: caller's column-major buffer
     }
     const Tile* tiles = H->d_tiles.as<Tile>() + L.first_tile;
+    const size_t li = size_t(&L - H->launches.data());
+    if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li], st));
     if (L.gen) {
       dim3 grid(unsigned(L.ntiles), unsigned((r + kBN_G - 1) / kBN_G));
       H->kfn_g<<<grid, kThreadsG, H->smem_g, st>>>(H->maps_g, tiles, H->d_groups.as<Group>(), H->d_terms.as<Term>(),
@@ -846,6 +856,7 @@ void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double*
       H->kfn_s<<<grid, kThreadsS, H->smem_s, st>>>(H->maps_s, tiles, H->d_groups.as<Group>(), H->d_terms.as<Term>(),
                                                     r, H->kp, cbase, ldc, cpanel);
     }
+    if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li + 1], st));
   }
   if (timed) {
     while (marked <= 2) GOFMM_CUDA(cudaEventRecord(H->ev[1 + marked++], st));
@@ -856,6 +867,9 @@ void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double*
 
 void fill_phase_times(gofmm_handle* H, gofmm_eval_stats* s) {
   GOFMM_CUDA(cudaEventSynchronize(H->ev[4]));
+  H->launch_ms.assign(H->launches.size(), 0.f);
+  for (size_t i = 0; i < H->launches.size(); ++i)
+    GOFMM_CUDA(cudaEventElapsedTime(&H->launch_ms[i], H->lev[2 * i], H->lev[2 * i + 1]));
   float t[4];
   for (int i = 0; i < 4; ++i) GOFMM_CUDA(cudaEventElapsedTime(&t[i], H->ev[i], H->ev[i + 1]));
   s->ms_permute = t[0];
@@ -898,6 +912,8 @@ int gofmm_create(const gofmm_tree_desc* desc, const gofmm_options* opts, gofmm_h
     GOFMM_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
     for (auto& e : H->ev) GOFMM_CUDA(cudaEventCreate(&e));
     build(H.get(), desc, opts);
+    H->lev.assign(2 * H->launches.size(), nullptr);
+    for (auto& e : H->lev) GOFMM_CUDA(cudaEventCreate(&e));
     *out = H.release();
   });
 }
@@ -908,6 +924,8 @@ int gofmm_destroy(gofmm_handle* H) {
     cudaSetDevice(H->device);
     cudaStreamSynchronize(H->stream);
     for (auto& e : H->ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : H->lev)
       if (e) cudaEventDestroy(e);
     if (H->stream) cudaStreamDestroy(H->stream);
     delete H;
@@ -920,6 +938,22 @@ int gofmm_phase_flops(const gofmm_handle* H, int32_t r, int64_t* out3) {
   return guarded([&] {
     if (!H || !out3) throw Error(GOFMM_ERR_INVALID, "null argument");
     for (int i = 0; i < 3; ++i) out3[i] = H->phase_flops_per_rhs[i] * int64_t(r);
+  });
+}
+
+int gofmm_launch_profile(const gofmm_handle* H, int32_t r, int32_t cap, gofmm_launch_info* out, int32_t* count) {
+  return guarded([&] {
+    if (!H || !count) throw Error(GOFMM_ERR_INVALID, "null argument");
+    *count = int32_t(H->launches.size());
+    for (int32_t i = 0; i < std::min<int32_t>(cap, *count); ++i) {
+      const Launch& L = H->launches[i];
+      out[i].phase = L.phase;
+      out[i].level = L.level;
+      out[i].ctas = int64_t(L.ntiles) * ((r + (L.gen ? kBN_G : kBN_S) - 1) / (L.gen ? kBN_G : kBN_S));
+      out[i].flops = L.flops_per_rhs * int64_t(r);
+      out[i].ms = i < int32_t(H->launch_ms.size()) ? H->launch_ms[i] : -1.0;
+      out[i].generated = L.gen ? 1 : 0;
+    }
   });
 }
 

@@ -166,6 +166,16 @@ class Evaluator:
         L.check(L.lib().gofmm_phase_flops(self._h, r, _p(out)))
         return dict(upward=int(out[0]), downward=int(out[1]), output=int(out[2]))
 
+    def launch_profile(self, r: int) -> list[dict]:
+        """Per-launch phase/level/flops and the CUDA-event ms of the last timed evaluation."""
+        n = C.c_int32()
+        L.check(L.lib().gofmm_launch_profile(self._h, r, 0, None, C.byref(n)))
+        arr = (L.LaunchInfo * max(n.value, 1))()
+        L.check(L.lib().gofmm_launch_profile(self._h, r, n.value, arr, C.byref(n)))
+        names = ("upward", "downward", "output")
+        return [dict(phase=names[x.phase], level=x.level, ctas=x.ctas, flops=x.flops, ms=x.ms,
+                     generated=bool(x.generated)) for x in arr[:n.value]]
+
     @property
     def launches_per_eval(self) -> int:
         return int(L.lib().gofmm_launches_per_eval(self._h))
