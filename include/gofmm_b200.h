@@ -98,7 +98,7 @@ typedef struct gofmm_options {
   int32_t device;     /* CUDA device ordinal */
   int32_t near_mode;  /* GOFMM_BLOCKS_* for D and near (S) blocks; default matrix-free */
   int32_t far_mode;   /* GOFMM_BLOCKS_* for far (coupling) blocks */
-  int32_t reserved;
+  int32_t max_rhs_chunk; /* columns per internal pass; 0 = as many as fit in free HBM */
 } gofmm_options;
 
 typedef struct gofmm_eval_stats {

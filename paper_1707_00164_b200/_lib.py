@@ -70,7 +70,7 @@ class TreeDesc(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("near_mode", C.c_int32), ("far_mode", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("max_rhs_chunk", C.c_int32)]
 
 
 class EvalStats(C.Structure):

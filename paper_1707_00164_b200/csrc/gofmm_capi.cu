@@ -224,7 +224,9 @@ struct gofmm_handle {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
   std::vector<cudaEvent_t> lev;  // per-launch start/stop events (timed evaluations only)
-  std::vector<float> launch_ms;  // durations of the last timed evaluation
+  std::vector<float> launch_ms;  // durations of the last timed evaluation (summed over chunks)
+  float phase_ms[4] = {0, 0, 0, 0};
+  int32_t max_chunk = 0;         // options.max_rhs_chunk (0 = size from free HBM)
   int32_t n = 0, num_nodes = 0, depth = 0, dim = 0, kernel = -1, source = 0;
   gofmm::KernelParams kp{};
   int near_mode = GOFMM_BLOCKS_MATRIX_FREE, far_mode = GOFMM_BLOCKS_MATRIX_FREE;
@@ -302,6 +304,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   if (o) {
     H->near_mode = o->near_mode;
     H->far_mode = o->far_mode;
+    H->max_chunk = o->max_rhs_chunk;
   }
   auto cp = [&](std::vector<int32_t>& v, const int32_t* p, int64_t k) { v.assign(p, p + k); };
   cp(H->parent, d->parent, nn);
@@ -386,8 +389,26 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   H->d_prow.upload(prow);
   H->d_iperm.upload(H->iperm);
 
-  // padded proj blob
-  {
+  // padded proj blob. When no node needs padding (even ranks, children ranks multiples of 16 —
+  // the saturated large trees) the caller's layout already is the device layout: one H2D copy,
+  // no host-side duplicate of a ~13-26 GB array.
+  bool proj_identity = true;
+  for (int i = 0; i < nn && proj_identity; ++i) {
+    const int k = H->rank[i];
+    if (k < 0) continue;
+    if (k % 2) proj_identity = false;
+    if (H->left[i] >= 0 && (H->rank[H->left[i]] % 16 || H->rank[H->right[i]] % 16)) proj_identity = false;
+    if (d->proj_offset[i] % 2) proj_identity = false;
+  }
+  if (proj_identity) {
+    H->proj_off.assign(nn, -1);
+    for (int i = 0; i < nn; ++i)
+      if (H->rank[i] >= 0) H->proj_off[i] = d->proj_offset[i];
+    const int64_t total = std::max<int64_t>(d->proj_offset[nn], 2);
+    H->d_proj.alloc(size_t(total) * sizeof(double), false);
+    if (d->proj_offset[nn] > 0)
+      GOFMM_CUDA(cudaMemcpy(H->d_proj.p, d->proj, size_t(d->proj_offset[nn]) * sizeof(double), cudaMemcpyHostToDevice));
+  } else {
     std::vector<double> blob;
     H->proj_off.assign(nn, -1);
     for (int i = 0; i < nn; ++i) {
@@ -808,9 +829,9 @@ int guarded(F&& f) {
   }
 }
 
-// Enqueue one evaluation on `st`: W (original order, device) -> u_perm (device).
-void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double* d_u, int64_t ldu, cudaStream_t st,
-             bool timed) {
+// Enqueue one column chunk of an evaluation on `st`: W (original order, device) -> u_perm (device).
+void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double* d_u, int64_t ldu,
+                   cudaStream_t st, bool timed) {
   ensure_workspace(H, r);
   upload_plan(H);
   if (H->maps_r != r) {
@@ -825,8 +846,10 @@ void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double*
   }
   if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[0], st));
   {
-    // K5: row gather into the padded leaf layout (evaluate.hpp:294-295)
-    const int cpb = 8;  // columns per block: keeps the gathered source columns L2-resident
+    // K5: row gather into the padded leaf layout (evaluate.hpp:294-295). Blocks walk all rows of
+    // cpb columns before the next columns (grid.x = rows), so the randomly gathered source
+    // columns (N * cpb * 8 bytes) stay L2-resident: each 32-byte sector is fetched from HBM once.
+    const int cpb = int(std::max<int64_t>(1, std::min<int64_t>(8, (48ll << 20) / (int64_t(H->n) * 8))));
     dim3 grid(unsigned((H->ld_wp + 255) / 256), unsigned((r + cpb - 1) / cpb));
     permute_rows_in<<<grid, 256, 0, st>>>(d_w, ldw, H->d_prow.as<int32_t>(), H->ld_wp, r, cpb,
                                           H->d_wp.as<double>(), int64_t(H->ws_r) * 16);
@@ -865,17 +888,58 @@ void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double*
   GOFMM_CUDA(cudaGetLastError());
 }
 
-void fill_phase_times(gofmm_handle* H, gofmm_eval_stats* s) {
+// add the event-measured phase / launch durations of the chunk just enqueued (timed mode)
+void accumulate_chunk_times(gofmm_handle* H) {
   GOFMM_CUDA(cudaEventSynchronize(H->ev[4]));
-  H->launch_ms.assign(H->launches.size(), 0.f);
-  for (size_t i = 0; i < H->launches.size(); ++i)
-    GOFMM_CUDA(cudaEventElapsedTime(&H->launch_ms[i], H->lev[2 * i], H->lev[2 * i + 1]));
-  float t[4];
-  for (int i = 0; i < 4; ++i) GOFMM_CUDA(cudaEventElapsedTime(&t[i], H->ev[i], H->ev[i + 1]));
-  s->ms_permute = t[0];
-  s->ms_upward = t[1];
-  s->ms_downward = t[2];
-  s->ms_output = t[3];
+  for (size_t i = 0; i < H->launches.size(); ++i) {
+    float ms;
+    GOFMM_CUDA(cudaEventElapsedTime(&ms, H->lev[2 * i], H->lev[2 * i + 1]));
+    H->launch_ms[i] += ms;
+  }
+  for (int i = 0; i < 4; ++i) {
+    float ms;
+    GOFMM_CUDA(cudaEventElapsedTime(&ms, H->ev[i], H->ev[i + 1]));
+    H->phase_ms[i] += ms;
+  }
+}
+
+// Column chunk for this r: evaluation is column-separable, so r beyond what the
+// workspace (W_perm + what + c, ~8*(ld_wp + 2*ld_s) bytes per column) fits in HBM is processed
+// in chunks (config 5: N = 2^22, r = 1024).
+int32_t rhs_chunk(gofmm_handle* H, int32_t r) {
+  if (H->max_chunk > 0) return std::min(r, H->max_chunk);
+  if (r <= H->ws_r) return r;
+  size_t free_b = 0, total_b = 0;
+  GOFMM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const double per_col = 8.0 * double(H->ld_wp + 2 * H->ld_s);
+  const double avail = 0.85 * double(free_b) + per_col * H->ws_r;  // current workspace is reusable
+  int64_t cols = int64_t(avail / per_col);
+  if (cols >= r) return r;
+  if (cols >= kBN_G) cols = (cols / kBN_G) * kBN_G;
+  if (cols < 1) throw Error(GOFMM_ERR_CUDA, "not enough device memory for one right-hand side");
+  return int32_t(cols);
+}
+
+// Enqueue a whole evaluation (all column chunks).
+void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double* d_u, int64_t ldu, cudaStream_t st,
+             bool timed) {
+  const int32_t rc = rhs_chunk(H, r);
+  if (timed) {
+    H->launch_ms.assign(H->launches.size(), 0.f);
+    std::fill(std::begin(H->phase_ms), std::end(H->phase_ms), 0.f);
+  }
+  for (int32_t c0 = 0; c0 < r; c0 += rc) {
+    const int32_t rr = std::min(rc, r - c0);
+    enqueue_chunk(H, d_w + size_t(c0) * ldw, ldw, rr, d_u + size_t(c0) * ldu, ldu, st, timed);
+    if (timed) accumulate_chunk_times(H);
+  }
+}
+
+void fill_phase_times(gofmm_handle* H, gofmm_eval_stats* s) {
+  s->ms_permute = H->phase_ms[0];
+  s->ms_upward = H->phase_ms[1];
+  s->ms_downward = H->phase_ms[2];
+  s->ms_output = H->phase_ms[3];
 }
 
 void check_args(gofmm_handle* H, const void* w, int64_t ldw, int32_t r, const void* u, int64_t ldu) {
@@ -994,30 +1058,51 @@ int gofmm_evaluate(gofmm_handle* H, const double* w, int64_t ldw, int32_t r, dou
     check_args(H, w, ldw, r, u_perm, ldu);
     GOFMM_CUDA(cudaSetDevice(H->device));
     auto t0 = std::chrono::steady_clock::now();
-    const size_t bytes = size_t(H->n) * r * sizeof(double);
+    cudaStream_t st = H->stream;
+    // device staging for W and u (a column chunk at a time when r does not fit)
+    const int32_t rc_ws = rhs_chunk(H, r);
+    size_t free_b = 0, total_b = 0;
+    GOFMM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t per_col = size_t(H->n) * sizeof(double);
+    int32_t rc = std::min<int32_t>(r, std::max<int32_t>(1, int32_t(std::min<size_t>(
+                                          size_t(rc_ws), (free_b / 2 + H->d_win.bytes) / (2 * per_col)))));
+    const size_t bytes = per_col * size_t(rc);
     if (H->d_win.bytes < bytes) {
       H->d_win.alloc(bytes, false);
       H->d_uout.alloc(bytes, false);
     }
-    cudaStream_t st = H->stream;
-    GOFMM_CUDA(cudaEventRecord(H->ev[5], st));
-    GOFMM_CUDA(cudaMemcpy2DAsync(H->d_win.p, size_t(H->n) * sizeof(double), w, size_t(ldw) * sizeof(double),
-                                 size_t(H->n) * sizeof(double), r, cudaMemcpyHostToDevice, st));
-    GOFMM_CUDA(cudaEventRecord(H->ev[6], st));
-    enqueue(H, H->d_win.as<double>(), H->n, r, H->d_uout.as<double>(), H->n, st, stats != nullptr);
-    GOFMM_CUDA(cudaMemcpy2DAsync(u_perm, size_t(ldu) * sizeof(double), H->d_uout.p, size_t(H->n) * sizeof(double),
-                                 size_t(H->n) * sizeof(double), r, cudaMemcpyDeviceToHost, st));
-    GOFMM_CUDA(cudaEventRecord(H->ev[7], st));
-    GOFMM_CUDA(cudaStreamSynchronize(st));
+    float h2d = 0, d2h = 0, ph[4] = {0, 0, 0, 0};
+    std::vector<float> lms(H->launches.size(), 0.f);
+    for (int32_t c0 = 0; c0 < r; c0 += rc) {
+      const int32_t rr = std::min(rc, r - c0);
+      GOFMM_CUDA(cudaEventRecord(H->ev[5], st));
+      GOFMM_CUDA(cudaMemcpy2DAsync(H->d_win.p, per_col, w + size_t(c0) * ldw, size_t(ldw) * sizeof(double), per_col,
+                                   rr, cudaMemcpyHostToDevice, st));
+      GOFMM_CUDA(cudaEventRecord(H->ev[6], st));
+      enqueue(H, H->d_win.as<double>(), H->n, rr, H->d_uout.as<double>(), H->n, st, stats != nullptr);
+      GOFMM_CUDA(cudaEventRecord(H->ev[4], st));
+      GOFMM_CUDA(cudaMemcpy2DAsync(u_perm + size_t(c0) * ldu, size_t(ldu) * sizeof(double), H->d_uout.p, per_col,
+                                   per_col, rr, cudaMemcpyDeviceToHost, st));
+      GOFMM_CUDA(cudaEventRecord(H->ev[7], st));
+      GOFMM_CUDA(cudaStreamSynchronize(st));
+      if (stats) {
+        float a, b;
+        GOFMM_CUDA(cudaEventElapsedTime(&a, H->ev[5], H->ev[6]));
+        GOFMM_CUDA(cudaEventElapsedTime(&b, H->ev[4], H->ev[7]));
+        h2d += a;
+        d2h += b;
+        for (int i = 0; i < 4; ++i) ph[i] += H->phase_ms[i];
+        for (size_t i = 0; i < lms.size(); ++i) lms[i] += H->launch_ms[i];
+      }
+    }
     if (stats) {
       std::memset(stats, 0, sizeof(*stats));
       stats->flops = H->flops_per_rhs * int64_t(r);
+      std::copy(ph, ph + 4, H->phase_ms);
+      H->launch_ms = lms;
       fill_phase_times(H, stats);
-      float a, b;
-      GOFMM_CUDA(cudaEventElapsedTime(&a, H->ev[5], H->ev[6]));
-      GOFMM_CUDA(cudaEventElapsedTime(&b, H->ev[4], H->ev[7]));
-      stats->ms_h2d = a;
-      stats->ms_d2h = b;
+      stats->ms_h2d = h2d;
+      stats->ms_d2h = d2h;
       stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
   });

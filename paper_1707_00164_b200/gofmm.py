@@ -95,7 +95,7 @@ class Evaluator:
     """A compressed tree resident on one B200, ready for repeated u = K~ W (gofmm_create)."""
 
     def __init__(self, tree: CompressedTree, device: int = 0, near_mode: int = L.BLOCKS_MATRIX_FREE,
-                 far_mode: int = L.BLOCKS_MATRIX_FREE, stored: bool | None = None):
+                 far_mode: int = L.BLOCKS_MATRIX_FREE, stored: bool | None = None, max_rhs_chunk: int = 0):
         self.tree = tree
         self.n = int(tree.n)
         lib = L.lib()
@@ -132,7 +132,7 @@ class Evaluator:
             d.coords = k(coords)
             for i, v in enumerate(tree.kparams[:4]):
                 d.kparam[i] = float(v)
-        o = L.Options(device, near_mode, far_mode, 0)
+        o = L.Options(device, near_mode, far_mode, max_rhs_chunk)
         h = C.c_void_p()
         L.check(lib.gofmm_create(C.byref(d), C.byref(o), C.byref(h)))
         self._h = h

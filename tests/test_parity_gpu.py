@@ -102,6 +102,20 @@ def test_rhs_counts(gpu, oracle, r):
     check_parity(gpu, oracle, h, r=r, modes=[dict(stored=False)])
 
 
+def test_rhs_chunking_matches(gpu, oracle):
+    """Column chunking (max_rhs_chunk) is invisible: evaluation is column-separable."""
+    pc = oracle.points_gaussian(700, 3, 5)
+    h = oracle.compress_kernel(oracle.GAUSSIAN, pc, 1.0, m=64, s=40, budget=0.05, seed=5)
+    tree = to_tree(h.export())
+    w = oracle.rng_gauss(700, 37, 1)
+    u_ref, _, _ = h.evaluate(w)
+    with gpu.Evaluator(tree, max_rhs_chunk=8) as ev:
+        p = ev.evaluate(w)
+    assert rel2(p.u, u_ref) <= TOL
+    with gpu.Evaluator(tree) as ev:
+        assert np.array_equal(ev.evaluate(w).u, p.u)
+
+
 def test_eps2_reproduces_reference(gpu, oracle):
     """error_eps2 (evaluate.hpp:330-373) on the criterion-2 fixture: 0.34486 (test_output.txt:21)."""
     n = 8192
