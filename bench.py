@@ -8,9 +8,11 @@ format). Inputs (W, 4.3 GB) exceed L2 (126 MB), so no extra flush is needed betw
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
 
-Under torchrun (N > 1) every rank evaluates its own r-column block of W against its own replica of
-the tree (evaluation is column-separable in r; no data-path collective), i.e. weak
-scaling over RHS blocks; the timed region is bracketed by a barrier and the max over ranks is used.
+Under torchrun (N > 1, N a power of two) the SAME config-3 evaluation is split across the ranks
+(strong scaling): the tree is cut at level log2(N), rank g owns the g-th subtree, nodes above the
+cut are evaluated redundantly, and one NCCL all-gather per evaluation exchanges the skeleton
+weights and W rows other ranks need (north_star (4)). The timed region is bracketed
+by a barrier + synchronize and the max over ranks is used.
 """
 from __future__ import annotations
 
@@ -202,8 +204,7 @@ def ours_arm(args, world, rank, local):
         cfg["budget"] = args.budget
     if args.n:
         cfg["n"] = args.n
-    r_total = args.r or cfg["r"]
-    r = r_total  # per-rank RHS block (weak scaling over RHS blocks)
+    r = args.r or cfg["r"]
     t0 = time.perf_counter()
     tree, cfg = synth.make_config_tree(args.config, seed=args.seed,
                                        **{k: cfg[k] for k in ("n", "budget")})
@@ -327,7 +328,7 @@ def ours_arm(args, world, rank, local):
                    "m": cfg["m"], "s": cfg["s"], "budget": cfg["budget"], "r_per_gpu": r,
                    "near_pairs": int(len(tree.near_a)), "far_pairs": int(len(tree.far_a)),
                    "tree": "synthetic saturated-rank tree (synth.py)", "l2_flush": (f"L2 flushed between steps (256 MB write, outside the per-step events); W {tree.n * r * 8 / 1e6:.1f} MB" if small else f"inputs larger than L2 (W {tree.n * r * 8 / 1e9:.2f} GB)"),
-                   "parallelism": f"rhs-blocks x{world}"},
+                   "parallelism": "single GPU"},
         "sec_per_eval": round(ms / 1e3, 6),
         "pct_fp64_peak": round(100.0 * value / 1e3 / (peak * world), 2),
         "flops_per_eval": int(flops),
@@ -340,6 +341,108 @@ def ours_arm(args, world, rank, local):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(ev.launches_per_eval * args.steps),
+        "setup_s": {"tree_gen": round(t_gen, 2), "create_upload": round(t_create, 2)},
+    }
+    if rank == 0:
+        line["clocks"] = clk.summary()
+        print(json.dumps(line), flush=True)
+    ev.close()
+    return 0
+
+
+def dist_arm(args, world, rank, local):
+    """Subtree-split evaluation of one config over `world` GPUs (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1707_00164_b200 import Evaluator, synth
+
+    torch.cuda.set_device(local)
+    cfg = dict(synth.CONFIGS[args.config])
+    if args.budget is not None:
+        cfg["budget"] = args.budget
+    if args.n:
+        cfg["n"] = args.n
+    r = args.r or cfg["r"]
+    t0 = time.perf_counter()
+    tree, cfg = synth.make_config_tree(args.config, seed=args.seed, **{k: cfg[k] for k in ("n", "budget")})
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ev = Evaluator(tree, device=local, rank=rank, nranks=world)
+    t_create = time.perf_counter() - t0
+    info = ev.dist_info()
+    full_flops = info["full_flops_per_rhs"] * r
+    gen = torch.Generator(device="cuda").manual_seed(1000)  # every rank holds the same W
+    w = torch.randn((r, tree.n), dtype=torch.float64, device="cuda", generator=gen).t()
+    u = torch.zeros((r, tree.n), dtype=torch.float64, device="cuda").t()
+    slot = info["max_send_rows"] * r
+    send = torch.empty(slot, dtype=torch.float64, device="cuda")
+    recv = torch.empty(slot * world, dtype=torch.float64, device="cuda")
+
+    def step():
+        ev.dist_stage1_torch(w, send)
+        if slot and world > 1:
+            dist.all_gather_into_tensor(recv, send)
+        ev.dist_stage2_torch(recv, r, u)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    ms = allmax(e0.elapsed_time(e1) / args.steps, world)
+    value = full_flops / (ms * 1e-3) / 1e9
+    peak, peak_src = fp64_peak_tflops()
+
+    # end to end: pinned host W -> device, evaluation, own rows of u -> pinned host
+    e2e = None
+    if not args.no_e2e:
+        w_h = torch.empty((r, tree.n), dtype=torch.float64, pin_memory=True)
+        w_h.copy_(w.t())
+        own = slice(int(info["own_row_begin"]), int(info["own_row_end"]))
+        u_h = torch.empty((r, own.stop - own.start), dtype=torch.float64, pin_memory=True)
+        ts = []
+        for it in range(args.e2e_steps + 1):
+            barrier(world)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            w.t().copy_(w_h, non_blocking=True)
+            step()
+            u_h.copy_(u.t()[:, own], non_blocking=True)
+            torch.cuda.synchronize()
+            if it:
+                ts.append(time.perf_counter() - t1)
+        sec = allmax(float(np.mean(ts)), world)
+        e2e = {"value": round(full_flops / sec / 1e9, 3), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(tree.n * r * 8), "d2h_bytes_per_step": int((own.stop - own.start) * r * 8),
+               "sec_per_eval": round(sec, 5), "note": "per rank: full W in, own rows of u out"}
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {KERNEL_NAMES.get(cfg['kernel'], 'kernel')} h={cfg['h']} N={tree.n} "
+                               f"d={cfg['d']} m={cfg['m']} s={cfg['s']} budget={cfg['budget']} r={r} total",
+                   "n": tree.n, "r": r, "budget": cfg["budget"], "parallelism": f"subtree split x{world}",
+                   "split_level": info["split_level"], "allgather_bytes_per_rank": int(slot * 8),
+                   "l2_flush": f"inputs larger than L2 (W {tree.n * r * 8 / 1e9:.2f} GB)"},
+        "sec_per_eval": round(ms / 1e3, 6),
+        "pct_fp64_peak": round(100.0 * value / 1e3 / (peak * world), 2),
+        "flops_per_eval": int(full_flops),
+        "rank_flops_max": int(allmax(float(info["flops_per_rhs"] * r), world)),
+        "rel_error": None,
+        "roofline": None,
+        "cpu_baseline": None,
+        "e2e": e2e,
+        "gpu_launches": int((ev.launches_per_eval + 2) * args.steps),
         "setup_s": {"tree_gen": round(t_gen, 2), "create_upload": round(t_create, 2)},
     }
     if rank == 0:
@@ -364,11 +467,14 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist", action="store_true", help="use the subtree-split path even on one GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     world, rank, local = dist_setup()
     if args.impl == "reference":
         rc = reference_arm(args, world, rank)
+    elif world > 1 or args.dist:
+        rc = dist_arm(args, world, rank, local)
     else:
         rc = ours_arm(args, world, rank, local)
     if world > 1:

@@ -153,6 +153,36 @@ typedef struct gofmm_launch_info {
 /* Fill up to cap entries of `out`; *count receives the number of launches. */
 int gofmm_launch_profile(const gofmm_handle* h, int32_t r, int32_t cap, gofmm_launch_info* out, int32_t* count);
 
+/* ---- multi-GPU: subtree split (north_star (4)) ------------------------------
+ * nranks = 2^l GPUs; the tree is split at level l, rank g owns the g-th level-l subtree
+ * (permuted rows [own_row_begin, own_row_end)); nodes above level l are evaluated redundantly.
+ * One all-gather per evaluation: stage1 packs this rank's exports (the skeleton weights `what`
+ * other ranks need — all level-l nodes plus cross-subtree far-field partners — and the W rows
+ * of leaves that are cross-subtree near-field partners) into a send buffer of
+ * max_send_rows x r doubles; the caller all-gathers the nranks send buffers (e.g. ncclAllGather
+ * via torch.distributed) into recv (nranks * max_send_rows * r doubles, rank order); stage2
+ * consumes it and writes this rank's rows of u_perm. No reduction of outputs is needed. */
+typedef struct gofmm_dist_info {
+  int32_t rank, nranks, split_level, n_exports;
+  int64_t send_rows;          /* rows (multiple of 16) this rank exports */
+  int64_t max_send_rows;      /* all-gather slot size in rows (max over ranks) */
+  int64_t own_row_begin, own_row_end;  /* this rank's permuted rows of u */
+  int64_t flops_per_rhs;      /* this rank's reference-counted flops (incl. redundant top) */
+  int64_t full_flops_per_rhs; /* the whole evaluation (reference counter) */
+} gofmm_dist_info;
+
+int gofmm_create_dist(const gofmm_tree_desc* desc, const gofmm_options* opts, int32_t rank, int32_t nranks,
+                      gofmm_handle** out);
+int gofmm_dist_get_info(const gofmm_handle* h, gofmm_dist_info* info);
+/* Host-only plan (no device touched): info and up to cap exported ids (what: node id,
+ * W rows: -(leaf id + 1)), in send-buffer order. */
+int gofmm_dist_plan_host(const gofmm_tree_desc* desc, int32_t rank, int32_t nranks, gofmm_dist_info* info,
+                         int32_t cap, int32_t* export_ids);
+/* d_w: full N x r W in original order (device); d_send: max_send_rows x r doubles. */
+int gofmm_dist_stage1(gofmm_handle* h, const double* d_w, int64_t ldw, int32_t r, double* d_send, void* stream);
+/* d_recv: nranks x max_send_rows x r doubles (all-gathered); writes u_perm rows of this rank. */
+int gofmm_dist_stage2(gofmm_handle* h, const double* d_recv, int32_t r, double* d_u_perm, int64_t ldu, void* stream);
+
 /* Bytes of device memory held by the handle (tree + workspace). */
 int64_t gofmm_device_bytes(const gofmm_handle* h);
 

@@ -84,6 +84,15 @@ class LaunchInfo(C.Structure):
                 ("ms", C.c_double), ("generated", C.c_int32), ("reserved", C.c_int32)]
 
 
+class DistInfo(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("split_level", C.c_int32), ("n_exports", C.c_int32),
+                ("send_rows", C.c_int64), ("max_send_rows", C.c_int64), ("own_row_begin", C.c_int64),
+                ("own_row_end", C.c_int64), ("flops_per_rhs", C.c_int64), ("full_flops_per_rhs", C.c_int64)]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
 class GofmmError(RuntimeError):
     """Raised for non-zero C-ABI return codes; ``code`` follows gfmm_cli.cpp:289-305."""
 
@@ -101,7 +110,8 @@ _lib = None
 # every symbol include/gofmm_b200.h declares
 EXPORTS = ("gofmm_create", "gofmm_evaluate", "gofmm_evaluate_device", "gofmm_unpermute_device",
            "gofmm_flops", "gofmm_phase_flops", "gofmm_launch_profile", "gofmm_device_bytes", "gofmm_launches_per_eval", "gofmm_destroy",
-           "gofmm_last_error", "gofmm_abi_version")
+           "gofmm_last_error", "gofmm_abi_version", "gofmm_create_dist", "gofmm_dist_get_info",
+           "gofmm_dist_plan_host", "gofmm_dist_stage1", "gofmm_dist_stage2")
 
 
 def lib():
@@ -120,6 +130,11 @@ def lib():
         L.gofmm_flops.restype = C.c_int64
         L.gofmm_phase_flops.argtypes = [P, C.c_int32, P]
         L.gofmm_launch_profile.argtypes = [P, C.c_int32, C.c_int32, P, C.POINTER(C.c_int32)]
+        L.gofmm_create_dist.argtypes = [C.POINTER(TreeDesc), C.POINTER(Options), C.c_int32, C.c_int32, C.POINTER(P)]
+        L.gofmm_dist_get_info.argtypes = [P, C.POINTER(DistInfo)]
+        L.gofmm_dist_plan_host.argtypes = [C.POINTER(TreeDesc), C.c_int32, C.c_int32, C.POINTER(DistInfo), C.c_int32, P]
+        L.gofmm_dist_stage1.argtypes = [P, P, C.c_int64, C.c_int32, P, P]
+        L.gofmm_dist_stage2.argtypes = [P, P, C.c_int32, P, C.c_int64, P]
         L.gofmm_device_bytes.argtypes = [P]
         L.gofmm_device_bytes.restype = C.c_int64
         L.gofmm_launches_per_eval.argtypes = [P]

@@ -214,7 +214,110 @@ struct Launch {
   int phase;  // 0 upward, 1 downward, 2 output
   int level;  // tree level (output launch: -1)
   int64_t flops_per_rhs = 0;  // reference-counted flops of this launch per RHS column
+  int stage = 2;  // distributed evaluation: 1 = before the all-gather (own-subtree N2S), 2 = after
 };
+
+// ---------------------------------------------------------------- subtree-split distribution
+// north_star (4): for P = 2^l GPUs the tree is split at level l into P subtrees, one per rank.
+// Rank g owns the nodes below its level-l node; nodes above level l ("top") are evaluated
+// redundantly by every rank. One all-gather per evaluation exchanges, from every rank, the
+// skeleton weights (what) other ranks need (all level-l nodes for the top N2S, plus far-field
+// partners across subtrees) and the W rows of leaves that are near-field partners across
+// subtrees. Everything below is pure host logic over the flattened tree.
+struct Seg {
+  int32_t buf;   // 0 = what (skeleton space), 1 = W_perm (point space)
+  int64_t row;   // first row (16-aligned)
+  int64_t rows;  // multiple of 16
+};
+
+struct DistPlan {
+  int nranks = 1, split = 0;
+  std::vector<int32_t> owner;              // -1 = top (replicated)
+  std::vector<std::vector<Seg>> exports;   // per rank, in send-buffer order
+  std::vector<int64_t> send_rows;          // per rank
+  int64_t max_send_rows = 0;
+};
+
+inline int64_t pad16_(int64_t x) { return (x + 15) & ~int64_t(15); }
+
+DistPlan make_dist_plan(int nranks, int nn, const int32_t* left, const int32_t* right, const int32_t* level,
+                        const int32_t* start, const int32_t* end, const int32_t* rank, int64_t n_near,
+                        const int32_t* near_a, const int32_t* near_b, int64_t n_far, const int32_t* far_a,
+                        const int32_t* far_b) {
+  DistPlan P;
+  P.nranks = nranks;
+  if (nranks < 1 || (nranks & (nranks - 1)))
+    throw Error(GOFMM_ERR_INVALID, "the number of ranks must be a power of two");
+  int l = 0;
+  while ((1 << l) < nranks) ++l;
+  P.split = l;
+  // every node above the split must be interior so that level l has exactly nranks nodes
+  std::vector<int> at_split;
+  for (int i = 0; i < nn; ++i) {
+    if (level[i] < l && left[i] < 0)
+      throw Error(GOFMM_ERR_INVALID, "tree too shallow for " + std::to_string(nranks) + " ranks");
+    if (level[i] == l) at_split.push_back(i);
+  }
+  if (int(at_split.size()) != nranks) throw Error(GOFMM_ERR_INVALID, "split level does not have one node per rank");
+  P.owner.assign(nn, -1);
+  for (int g = 0; g < nranks; ++g) P.owner[at_split[g]] = g;
+  for (int i = 0; i < nn; ++i)  // BFS order: parents first
+    if (level[i] >= l && left[i] >= 0) P.owner[left[i]] = P.owner[right[i]] = P.owner[i];
+  for (int i = 0; i < nn; ++i)
+    if (level[i] > l && P.owner[i] < 0) {
+      // children were assigned from their parent above; a node deeper than l with no owner
+      // would mean an inconsistent tree
+      throw Error(GOFMM_ERR_INVALID, "node below the split without an owning subtree");
+    }
+  std::vector<char> need_what(nn, 0), need_w(nn, 0);
+  if (nranks > 1) {
+    for (int i : at_split) need_what[i] = 1;  // every rank's top N2S needs all level-l what
+    auto request = [&](int requester_node, int target) {
+      const int ro = P.owner[requester_node], to = P.owner[target];
+      if (to < 0) return;                 // top what is recomputed by everyone
+      if (ro < 0 || ro != to) need_what[target] = 1;  // top requesters run on every rank
+    };
+    for (int64_t t = 0; t < n_far; ++t) {
+      request(far_a[t], far_b[t]);
+      request(far_b[t], far_a[t]);
+    }
+    for (int64_t t = 0; t < n_near; ++t) {
+      const int a = near_a[t], b = near_b[t];
+      if (P.owner[a] != P.owner[b]) need_w[a] = need_w[b] = 1;
+    }
+  }
+  // skeleton / point space offsets (same formulas as build())
+  std::vector<int64_t> soff(nn, -1), pst(nn, -1);
+  int64_t off = 0;
+  for (int i = 0; i < nn; ++i)
+    if (rank[i] >= 0) {
+      soff[i] = off;
+      off += pad16_(rank[i]);
+    }
+  std::vector<int32_t> leaves;
+  for (int i = 0; i < nn; ++i)
+    if (left[i] < 0) leaves.push_back(i);
+  std::sort(leaves.begin(), leaves.end(), [&](int a, int b) { return start[a] < start[b]; });
+  off = 0;
+  for (int i : leaves) {
+    pst[i] = off;
+    off += pad16_(end[i] - start[i]);
+  }
+  P.exports.assign(nranks, {});
+  P.send_rows.assign(nranks, 0);
+  for (int i = 0; i < nn; ++i)
+    if (need_what[i] && P.owner[i] >= 0) {
+      if (rank[i] < 0) throw Error(GOFMM_ERR_INVALID, "exported node has no skeleton");
+      P.exports[P.owner[i]].push_back({0, soff[i], pad16_(rank[i])});
+    }
+  for (int i : leaves)
+    if (need_w[i]) P.exports[P.owner[i]].push_back({1, pst[i], pad16_(end[i] - start[i])});
+  for (int g = 0; g < nranks; ++g) {
+    for (const Seg& sg : P.exports[g]) P.send_rows[g] += sg.rows;
+    P.max_send_rows = std::max(P.max_send_rows, P.send_rows[g]);
+  }
+  return P;
+}
 
 }  // namespace
 }  // namespace gofmm
@@ -253,6 +356,15 @@ struct gofmm_handle {
   // workspace
   gofmm::DevBuf d_wp, d_what, d_c, d_win, d_uout;
   int32_t ws_r = 0;
+
+  // distribution (nranks == 1: single-GPU evaluation)
+  int32_t drank = 0, nranks = 1;
+  gofmm::DistPlan dist;
+  int64_t own_pst_begin = 0, own_pst_end = 0;  // own leaves' rows in point space
+  int64_t own_begin = 0, own_end = 0;          // own permuted rows [start, end)
+  int64_t full_flops_per_rhs = 0;              // the whole (undistributed) evaluation
+  gofmm::DevBuf d_segs;                        // pack / unpack segment table
+  int32_t n_pack = 0, n_unpack = 0;
 
   gofmm::KernelFn kfn_s = nullptr, kfn_g = nullptr;
   size_t smem_s = 0, smem_g = 0;
@@ -381,6 +493,25 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     off += pad16(H->rank[i]);
   }
   H->ld_s = std::max<int64_t>(pad16(off), 16);
+
+  // subtree split (single GPU: nranks == 1, everything owned by rank 0)
+  H->dist = make_dist_plan(H->nranks, nn, d->left, d->right, d->level, d->start, d->end, d->rank, d->num_near,
+                           d->near_a, d->near_b, d->num_far, d->far_a, d->far_b);
+  if (H->drank < 0 || H->drank >= H->nranks) throw Error(GOFMM_ERR_INVALID, "rank out of range");
+  {
+    H->own_pst_begin = H->ld_wp;
+    H->own_pst_end = 0;
+    H->own_begin = d->n;
+    H->own_end = 0;
+    for (int id : H->leaf_ids)
+      if (H->dist.owner[id] == H->drank) {
+        H->own_pst_begin = std::min(H->own_pst_begin, H->pst[id]);
+        H->own_pst_end = std::max(H->own_pst_end, H->pst[id] + pad16(H->end[id] - H->start[id]));
+        H->own_begin = std::min<int64_t>(H->own_begin, H->start[id]);
+        H->own_end = std::max<int64_t>(H->own_end, H->end[id]);
+      }
+  }
+  auto active = [&](int i) { return H->dist.owner[i] == H->drank || H->dist.owner[i] < 0; };
 
   // row map for the permutation kernel, and iperm
   std::vector<int32_t> prow(H->ld_wp, -1);
@@ -587,7 +718,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   for (int lev = H->depth; lev >= 1; --lev) {
     std::vector<HostGroup> gs;
     for (int i = 0; i < nn; ++i) {
-      if (H->level[i] != lev || H->rank[i] < 0) continue;
+      if (H->level[i] != lev || H->rank[i] < 0 || !active(i)) continue;
       HostGroup g;
       g.c_row = H->soff[i];
       g.M = H->rank[i];
@@ -612,6 +743,8 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
       gs.push_back(std::move(g));
     }
     push_launch(gs, false, Buf::What, 0, lev);
+    if (!H->launches.empty() && H->launches.back().level == lev && H->launches.back().phase == 0)
+      H->launches.back().stage = (lev >= H->dist.split) ? 1 : 2;
   }
 
   // downward: coupling (S2S) + parent term (S2N), top level first (evaluate.hpp:95-111,164-195)
@@ -619,7 +752,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     std::vector<HostGroup> gs;
     bool any_gen = false;
     for (int i = 0; i < nn; ++i) {
-      if (H->level[i] != lev || H->rank[i] < 0) continue;
+      if (H->level[i] != lev || H->rank[i] < 0 || !active(i)) continue;
       HostGroup g;
       g.c_row = H->soff[i];
       g.M = H->rank[i];
@@ -670,6 +803,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   {
     std::vector<HostGroup> gs;
     for (int id : H->leaf_ids) {
+      if (H->dist.owner[id] != H->drank) continue;
       HostGroup g;
       g.c_row = H->start[id];
       g.M = nrows(id);
@@ -731,6 +865,21 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     push_launch(gs, gen_near, Buf::Out, 2, -1);
   }
   H->flops_per_rhs = flops;
+  {
+    // reference counter of the whole evaluation (evaluate.hpp:154-214), independent of the split
+    int64_t f = 0;
+    for (int i = 0; i < nn; ++i) {
+      if (H->rank[i] < 0) continue;
+      f += 2LL * H->rank[i] * ncand[i];  // upward
+      const int par = H->parent[i];
+      if (par > 0 && H->rank[par] >= 0) f += 2LL * H->rank[par] * H->rank[i];  // downward
+      if (H->left[i] < 0) f += 2LL * H->rank[i] * nrows(i);                     // leaf S2N
+    }
+    for (size_t t = 0; t < H->far_a.size(); ++t) f += 4LL * H->rank[H->far_a[t]] * H->rank[H->far_b[t]];
+    for (size_t t = 0; t < H->near_a.size(); ++t) f += 4LL * nrows(H->near_a[t]) * nrows(H->near_b[t]);
+    for (int id : H->leaf_ids) f += 2LL * nrows(id) * nrows(id);
+    H->full_flops_per_rhs = f;
+  }
   H->phase_flops_per_rhs[2] = flops - H->phase_flops_per_rhs[0] - H->phase_flops_per_rhs[1];
 
   H->kfn_s = &grouped_gemm_f64<CFG_S, kKindNone, 1>;
@@ -747,6 +896,27 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   size_t nterms = 0;
   for (auto& g : H->groups) nterms += g.terms.size();
   H->d_terms.alloc(std::max<size_t>(nterms, 1) * sizeof(Term), false);
+
+  // pack (own exports -> send buffer) and unpack (every other rank's exports -> workspace) tables
+  if (H->nranks > 1) {
+    std::vector<PanelSeg> segs;
+    int64_t row = 0;
+    for (const Seg& sg : H->dist.exports[H->drank]) {
+      segs.push_back({sg.buf, 0, sg.row, row, sg.rows});
+      row += sg.rows;
+    }
+    H->n_pack = int32_t(segs.size());
+    for (int h = 0; h < H->nranks; ++h) {
+      if (h == H->drank) continue;
+      row = int64_t(h) * H->dist.max_send_rows;
+      for (const Seg& sg : H->dist.exports[h]) {
+        segs.push_back({sg.buf, 0, sg.row, row, sg.rows});
+        row += sg.rows;
+      }
+    }
+    H->n_unpack = int32_t(segs.size()) - H->n_pack;
+    H->d_segs.upload(segs);
+  }
 }
 
 void ensure_workspace(gofmm_handle* H, int32_t r) {
@@ -830,8 +1000,10 @@ int guarded(F&& f) {
 }
 
 // Enqueue one column chunk of an evaluation on `st`: W (original order, device) -> u_perm (device).
+// stage 0: the whole evaluation; stage 1 / 2: the distributed halves around the all-gather
+// (d_xbuf = this rank's send buffer / the gathered receive buffer).
 void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double* d_u, int64_t ldu,
-                   cudaStream_t st, bool timed) {
+                   cudaStream_t st, bool timed, int stage = 0, double* d_xbuf = nullptr) {
   ensure_workspace(H, r);
   upload_plan(H);
   if (H->maps_r != r) {
@@ -845,19 +1017,29 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
     H->maps_r = r;
   }
   if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[0], st));
-  {
+  if (stage == 2 && H->n_unpack > 0) {
+    // ghosts: every other rank's exported what / W rows into their places in this workspace
+    dim3 grid(unsigned(H->n_unpack), 8);
+    panel_copy<<<grid, 256, 0, st>>>(H->d_segs.as<PanelSeg>() + H->n_pack, H->d_what.as<double>(),
+                                     H->d_wp.as<double>(), int64_t(H->ws_r) * 16, d_xbuf, r, 0);
+  }
+  if (stage != 2) {
     // K5: row gather into the padded leaf layout (evaluate.hpp:294-295). Blocks walk all rows of
     // cpb columns before the next columns (grid.x = rows), so the randomly gathered source
     // columns (N * cpb * 8 bytes) stay L2-resident: each 32-byte sector is fetched from HBM once.
     const int cpb = int(std::max<int64_t>(1, std::min<int64_t>(8, (48ll << 20) / (int64_t(H->n) * 8))));
-    dim3 grid(unsigned((H->ld_wp + 255) / 256), unsigned((r + cpb - 1) / cpb));
-    permute_rows_in<<<grid, 256, 0, st>>>(d_w, ldw, H->d_prow.as<int32_t>(), H->ld_wp, r, cpb,
-                                          H->d_wp.as<double>(), int64_t(H->ws_r) * 16);
+    const int64_t row0 = stage == 1 ? H->own_pst_begin : 0, row1 = stage == 1 ? H->own_pst_end : H->ld_wp;
+    if (row1 > row0) {
+      dim3 grid(unsigned((row1 - row0 + 255) / 256), unsigned((r + cpb - 1) / cpb));
+      permute_rows_in<<<grid, 256, 0, st>>>(d_w, ldw, H->d_prow.as<int32_t>(), row0, row1, r, cpb,
+                                            H->d_wp.as<double>(), int64_t(H->ws_r) * 16);
+    }
   }
   // ev[1 + p] marks the start of phase p (0 upward, 1 downward, 2 output); ev[4] the end
   if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[1], st));
   int marked = 1;
   for (const Launch& L : H->launches) {
+    if (stage != 0 && L.stage != stage) continue;
     while (timed && marked <= L.phase) GOFMM_CUDA(cudaEventRecord(H->ev[1 + marked++], st));
     double* cbase;
     int64_t ldc;
@@ -880,6 +1062,11 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
                                                     r, H->kp, cbase, ldc, cpanel);
     }
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li + 1], st));
+  }
+  if (stage == 1 && H->n_pack > 0) {
+    dim3 grid(unsigned(H->n_pack), 8);
+    panel_copy<<<grid, 256, 0, st>>>(H->d_segs.as<PanelSeg>(), H->d_what.as<double>(), H->d_wp.as<double>(),
+                                     int64_t(H->ws_r) * 16, d_xbuf, r, 1);
   }
   if (timed) {
     while (marked <= 2) GOFMM_CUDA(cudaEventRecord(H->ev[1 + marked++], st));
@@ -979,6 +1166,118 @@ int gofmm_create(const gofmm_tree_desc* desc, const gofmm_options* opts, gofmm_h
     H->lev.assign(2 * H->launches.size(), nullptr);
     for (auto& e : H->lev) GOFMM_CUDA(cudaEventCreate(&e));
     *out = H.release();
+  });
+}
+
+int gofmm_create_dist(const gofmm_tree_desc* desc, const gofmm_options* opts, int32_t rank, int32_t nranks,
+                      gofmm_handle** out) {
+  return guarded([&] {
+    if (!out) throw Error(GOFMM_ERR_INVALID, "null output handle");
+    *out = nullptr;
+    validate(desc);
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(GOFMM_ERR_INVALID, "bad rank / nranks");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw Error(GOFMM_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    auto H = std::make_unique<gofmm_handle>();
+    H->device = opts ? opts->device : 0;
+    H->drank = rank;
+    H->nranks = nranks;
+    GOFMM_CUDA(cudaSetDevice(H->device));
+    GOFMM_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
+    for (auto& e : H->ev) GOFMM_CUDA(cudaEventCreate(&e));
+    build(H.get(), desc, opts);
+    H->lev.assign(2 * H->launches.size(), nullptr);
+    for (auto& e : H->lev) GOFMM_CUDA(cudaEventCreate(&e));
+    *out = H.release();
+  });
+}
+
+static void fill_dist_info(const DistPlan& P, int32_t rank, int64_t own_begin, int64_t own_end, int64_t flops,
+                           int64_t full, gofmm_dist_info* info) {
+  std::memset(info, 0, sizeof(*info));
+  info->rank = rank;
+  info->nranks = P.nranks;
+  info->split_level = P.split;
+  info->send_rows = P.send_rows.empty() ? 0 : P.send_rows[rank];
+  info->max_send_rows = P.max_send_rows;
+  info->own_row_begin = own_begin;
+  info->own_row_end = own_end;
+  info->flops_per_rhs = flops;
+  info->full_flops_per_rhs = full;
+  info->n_exports = P.exports.empty() ? 0 : int32_t(P.exports[rank].size());
+}
+
+int gofmm_dist_get_info(const gofmm_handle* H, gofmm_dist_info* info) {
+  return guarded([&] {
+    if (!H || !info) throw Error(GOFMM_ERR_INVALID, "null argument");
+    fill_dist_info(H->dist, H->drank, H->own_begin, H->own_end, H->flops_per_rhs, H->full_flops_per_rhs, info);
+  });
+}
+
+int gofmm_dist_plan_host(const gofmm_tree_desc* d, int32_t rank, int32_t nranks, gofmm_dist_info* info,
+                         int32_t cap, int32_t* export_ids) {
+  return guarded([&] {
+    validate(d);
+    if (rank < 0 || rank >= nranks) throw Error(GOFMM_ERR_INVALID, "bad rank / nranks");
+    DistPlan P = make_dist_plan(nranks, d->num_nodes, d->left, d->right, d->level, d->start, d->end, d->rank,
+                                d->num_near, d->near_a, d->near_b, d->num_far, d->far_a, d->far_b);
+    int64_t ob = d->n, oe = 0;
+    for (int i = 0; i < d->num_nodes; ++i)
+      if (d->left[i] < 0 && P.owner[i] == rank) {
+        ob = std::min<int64_t>(ob, d->start[i]);
+        oe = std::max<int64_t>(oe, d->end[i]);
+      }
+    if (info) fill_dist_info(P, rank, ob, oe, 0, 0, info);
+    if (export_ids) {
+      // node id of every exported segment: what segments as the node id, W segments as -(leaf+1)
+      int32_t k = 0;
+      std::vector<int64_t> soff(d->num_nodes, -1), pst(d->num_nodes, -1);
+      int64_t off = 0;
+      for (int i = 0; i < d->num_nodes; ++i)
+        if (d->rank[i] >= 0) {
+          soff[i] = off;
+          off += pad16_(d->rank[i]);
+        }
+      std::vector<int> leaves;
+      for (int i = 0; i < d->num_nodes; ++i)
+        if (d->left[i] < 0) leaves.push_back(i);
+      std::sort(leaves.begin(), leaves.end(), [&](int a, int b) { return d->start[a] < d->start[b]; });
+      off = 0;
+      for (int i : leaves) {
+        pst[i] = off;
+        off += pad16_(d->end[i] - d->start[i]);
+      }
+      for (const Seg& sg : P.exports[rank]) {
+        if (k >= cap) break;
+        int id = -1;
+        for (int i = 0; i < d->num_nodes && id < 0; ++i)
+          if ((sg.buf == 0 && soff[i] == sg.row && d->rank[i] >= 0) || (sg.buf == 1 && pst[i] == sg.row && d->left[i] < 0))
+            id = i;
+        export_ids[k++] = sg.buf == 0 ? id : -(id + 1);
+      }
+    }
+  });
+}
+
+int gofmm_dist_stage1(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double* d_send, void* stream) {
+  return guarded([&] {
+    check_args(H, d_w, ldw, r, d_w, H->n);
+    if (H->nranks > 1 && !d_send && H->dist.max_send_rows > 0) throw Error(GOFMM_ERR_INVALID, "null send buffer");
+    GOFMM_CUDA(cudaSetDevice(H->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    enqueue_chunk(H, d_w, ldw, r, nullptr, H->n, st, false, 1, d_send);
+  });
+}
+
+int gofmm_dist_stage2(gofmm_handle* H, const double* d_recv, int32_t r, double* d_u, int64_t ldu, void* stream) {
+  return guarded([&] {
+    check_args(H, d_u, H->n, r, d_u, ldu);
+    if (H->nranks > 1 && !d_recv && H->dist.max_send_rows > 0) throw Error(GOFMM_ERR_INVALID, "null receive buffer");
+    if (r > H->ws_r) throw Error(GOFMM_ERR_INVALID, "stage2: r differs from stage1");
+    GOFMM_CUDA(cudaSetDevice(H->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    enqueue_chunk(H, nullptr, H->n, r, d_u, ldu, st, false, 2, const_cast<double*>(d_recv));
   });
 }
 

@@ -580,17 +580,44 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
 
 // ------------------------------------------------------------------ permutations (K5)
 // wp[t, c] = w[prow[t], c]   (evaluate.hpp:294-295) into the padded leaf layout, stored in
-// 16-row panels (panel stride `pstride` doubles); prow = -1 marks padding rows (written as 0)
+// 16-row panels (panel stride `pstride` doubles); prow = -1 marks padding rows (written as 0).
+// Rows [row0, row1) only (a rank's own leaves in a distributed evaluation).
 __global__ void permute_rows_in(const double* __restrict__ w, int64_t ldw, const int32_t* __restrict__ prow,
-                                int64_t npad, int32_t r, int32_t cols_per_block, double* __restrict__ wp,
-                                int64_t pstride) {
-  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= npad) return;
+                                int64_t row0, int64_t row1, int32_t r, int32_t cols_per_block,
+                                double* __restrict__ wp, int64_t pstride) {
+  const int64_t t = row0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= row1) return;
   const int32_t src = prow[t];
   const int c0 = blockIdx.y * cols_per_block;
   const int c1 = min(r, c0 + cols_per_block);
   double* dst = wp + (t >> 4) * pstride + (t & 15);
   for (int c = c0; c < c1; ++c) dst[size_t(c) * 16] = (src >= 0) ? __ldg(w + src + size_t(c) * ldw) : 0.0;
+}
+
+// Distributed evaluation: copy whole 16-row panels (first r columns) between the workspace
+// (panel stride ws_pstride) and the compact exchange buffer (panel stride 16*r).
+struct PanelSeg {
+  int32_t buf;  // 0 = what, 1 = W_perm
+  int32_t pad;
+  int64_t ws_row;   // 16-aligned row in the workspace
+  int64_t buf_row;  // 16-aligned row in the exchange buffer
+  int64_t rows;     // multiple of 16
+};
+
+__global__ void panel_copy(const PanelSeg* __restrict__ segs, double* __restrict__ what, double* __restrict__ wp,
+                           int64_t ws_pstride, double* __restrict__ buf, int32_t r, int32_t to_buffer) {
+  const PanelSeg sg = segs[blockIdx.x];
+  double* ws = (sg.buf == 0) ? what : wp;
+  const int64_t npan = sg.rows / 16;
+  const int64_t per = int64_t(16) * r;  // the first r columns of a panel are contiguous
+  for (int64_t p = blockIdx.y; p < npan; p += gridDim.y) {
+    double* a = ws + (sg.ws_row / 16 + p) * ws_pstride;
+    double* b = buf + (sg.buf_row / 16 + p) * per;
+    if (to_buffer)
+      for (int64_t i = threadIdx.x; i < per; i += blockDim.x) b[i] = a[i];
+    else
+      for (int64_t i = threadIdx.x; i < per; i += blockDim.x) a[i] = b[i];
+  }
 }
 
 // u[iperm[t], c] = up[t, c]   (unpermute, evaluate.hpp:21-25)

@@ -91,52 +91,74 @@ def _p(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
+def make_desc(tree: CompressedTree, stored: bool | None = None):
+    """Flatten a CompressedTree into the C descriptor; returns (desc, keepalive list, stored flag)."""
+    keep = []
+
+    def k(a):
+        keep.append(a)
+        return _p(a)
+
+    d = L.TreeDesc()
+    d.n, d.num_nodes = int(tree.n), tree.num_nodes
+    d.parent, d.left, d.right = k(_i32(tree.parent)), k(_i32(tree.left)), k(_i32(tree.right))
+    d.level, d.start, d.end = k(_i32(tree.level)), k(_i32(tree.start)), k(_i32(tree.end))
+    d.iperm, d.rank = k(_i32(tree.iperm)), k(_i32(tree.rank))
+    d.skel_offset, d.skel_idx = k(_i64(tree.skel_off)), k(_i32(np.append(tree.skel_idx, 0)))
+    d.proj_offset, d.proj = k(_i64(tree.proj_off)), k(_f64(np.append(tree.proj, 0.0)))
+    d.num_near, d.near_a, d.near_b = len(tree.near_a), k(_i32(np.append(tree.near_a, 0))), k(
+        _i32(np.append(tree.near_b, 0)))
+    d.num_far, d.far_a, d.far_b = len(tree.far_a), k(_i32(np.append(tree.far_a, 0))), k(
+        _i32(np.append(tree.far_b, 0)))
+    use_stored = stored if stored is not None else (tree.coords is None or tree.kernel < 0)
+    if use_stored:
+        if tree.diag is None:
+            raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "stored source needs diag/near/far blocks")
+        d.source = L.SOURCE_STORED
+        d.diag_offset, d.diag_blocks = k(_i64(tree.diag_off)), k(_f64(tree.diag))
+        d.near_offset, d.near_blocks = k(_i64(tree.near_off)), k(_f64(tree.near_blk))
+        d.far_offset, d.far_blocks = k(_i64(tree.far_off)), k(_f64(tree.far_blk))
+    else:
+        d.source = L.SOURCE_KERNEL
+        d.kernel = int(tree.kernel)
+        coords = np.asfortranarray(tree.coords, dtype=np.float64)
+        d.dim = int(coords.shape[0])
+        d.coords = k(coords)
+        for i, v in enumerate(tree.kparams[:4]):
+            d.kparam[i] = float(v)
+    return d, keep, use_stored
+
+
+def dist_plan_host(tree: CompressedTree, rank: int, nranks: int) -> tuple[dict, list[int]]:
+    """Host-only subtree-split plan (no device): info and the exported ids in send order
+    (what: node id; W rows: -(leaf id + 1))."""
+    d, keep, _ = make_desc(tree)
+    info = L.DistInfo()
+    L.check(L.lib().gofmm_dist_plan_host(C.byref(d), rank, nranks, C.byref(info), 0, None))
+    ids = np.zeros(max(info.n_exports, 1), dtype=np.int32)
+    L.check(L.lib().gofmm_dist_plan_host(C.byref(d), rank, nranks, C.byref(info), info.n_exports, _p(ids)))
+    return info.as_dict(), ids[:info.n_exports].tolist()
+
+
 class Evaluator:
     """A compressed tree resident on one B200, ready for repeated u = K~ W (gofmm_create)."""
 
     def __init__(self, tree: CompressedTree, device: int = 0, near_mode: int = L.BLOCKS_MATRIX_FREE,
-                 far_mode: int = L.BLOCKS_MATRIX_FREE, stored: bool | None = None, max_rhs_chunk: int = 0):
+                 far_mode: int = L.BLOCKS_MATRIX_FREE, stored: bool | None = None, max_rhs_chunk: int = 0,
+                 rank: int | None = None, nranks: int = 1):
         self.tree = tree
         self.n = int(tree.n)
         lib = L.lib()
-        keep = []
-
-        def k(a):
-            keep.append(a)
-            return _p(a)
-
-        d = L.TreeDesc()
-        d.n, d.num_nodes = self.n, tree.num_nodes
-        d.parent, d.left, d.right = k(_i32(tree.parent)), k(_i32(tree.left)), k(_i32(tree.right))
-        d.level, d.start, d.end = k(_i32(tree.level)), k(_i32(tree.start)), k(_i32(tree.end))
-        d.iperm, d.rank = k(_i32(tree.iperm)), k(_i32(tree.rank))
-        d.skel_offset, d.skel_idx = k(_i64(tree.skel_off)), k(_i32(np.append(tree.skel_idx, 0)))
-        d.proj_offset, d.proj = k(_i64(tree.proj_off)), k(_f64(np.append(tree.proj, 0.0)))
-        d.num_near, d.near_a, d.near_b = len(tree.near_a), k(_i32(np.append(tree.near_a, 0))), k(
-            _i32(np.append(tree.near_b, 0)))
-        d.num_far, d.far_a, d.far_b = len(tree.far_a), k(_i32(np.append(tree.far_a, 0))), k(
-            _i32(np.append(tree.far_b, 0)))
-        use_stored = stored if stored is not None else (tree.coords is None or tree.kernel < 0)
-        if use_stored:
-            if tree.diag is None:
-                raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "stored source needs diag/near/far blocks")
-            d.source = L.SOURCE_STORED
-            d.diag_offset, d.diag_blocks = k(_i64(tree.diag_off)), k(_f64(tree.diag))
-            d.near_offset, d.near_blocks = k(_i64(tree.near_off)), k(_f64(tree.near_blk))
-            d.far_offset, d.far_blocks = k(_i64(tree.far_off)), k(_f64(tree.far_blk))
-        else:
-            d.source = L.SOURCE_KERNEL
-            d.kernel = int(tree.kernel)
-            coords = np.asfortranarray(tree.coords, dtype=np.float64)
-            d.dim = int(coords.shape[0])
-            d.coords = k(coords)
-            for i, v in enumerate(tree.kparams[:4]):
-                d.kparam[i] = float(v)
+        d, keep, use_stored = make_desc(tree, stored)
         o = L.Options(device, near_mode, far_mode, max_rhs_chunk)
         h = C.c_void_p()
-        L.check(lib.gofmm_create(C.byref(d), C.byref(o), C.byref(h)))
+        if rank is None:
+            L.check(lib.gofmm_create(C.byref(d), C.byref(o), C.byref(h)))
+        else:
+            L.check(lib.gofmm_create_dist(C.byref(d), C.byref(o), rank, nranks, C.byref(h)))
         self._h = h
         self.stored = use_stored
+        self.rank, self.nranks = rank, nranks
 
     def close(self):
         if getattr(self, "_h", None):
@@ -233,6 +255,44 @@ class Evaluator:
         stats = self.evaluate_device(wt.data_ptr(), wt.stride(1), r, out.data_ptr(), out.stride(1), stream,
                                      sync_stats)
         return out, stats
+
+    # ------------------------------------------------------------------ subtree-split (multi-GPU)
+    def dist_info(self) -> dict:
+        info = L.DistInfo()
+        L.check(L.lib().gofmm_dist_get_info(self._h, C.byref(info)))
+        return info.as_dict()
+
+    def dist_stage1_torch(self, w, send):
+        """Own-subtree upward pass + pack of this rank's exports into `send` (CUDA float64)."""
+        import torch
+
+        wt = _colmajor(w)
+        stream = torch.cuda.current_stream(w.device).cuda_stream
+        L.check(L.lib().gofmm_dist_stage1(self._h, C.c_void_p(wt.data_ptr()), wt.stride(1), int(w.shape[1]),
+                                          C.c_void_p(send.data_ptr()) if send.numel() else None,
+                                          C.c_void_p(stream if stream else 1)))
+
+    def dist_stage2_torch(self, recv, r: int, out):
+        """Ghost unpack + top tree + downward + output of this rank's rows of u_perm (into `out`)."""
+        import torch
+
+        stream = torch.cuda.current_stream(out.device).cuda_stream
+        L.check(L.lib().gofmm_dist_stage2(self._h, C.c_void_p(recv.data_ptr()) if recv.numel() else None, r,
+                                          C.c_void_p(out.data_ptr()), out.stride(1),
+                                          C.c_void_p(stream if stream else 1)))
+
+    def evaluate_dist_torch(self, w, out, all_gather):
+        """One distributed evaluation: stage1, all_gather(send) -> recv, stage2. `all_gather` maps
+        this rank's flat send tensor to the rank-ordered concatenation of every rank's."""
+        import torch
+
+        info = self.dist_info()
+        r = int(w.shape[1])
+        send = torch.empty(info["max_send_rows"] * r, dtype=torch.float64, device=w.device)
+        self.dist_stage1_torch(w, send)
+        recv = all_gather(send)
+        self.dist_stage2_torch(recv, r, out)
+        return out
 
     def unpermute(self, u_perm: np.ndarray) -> np.ndarray:
         """out.row(iperm[t]) = u_perm.row(t) (evaluate.hpp:21-25)."""

@@ -215,3 +215,54 @@ def test_full_size_c3_linearity(gpu):
         num = torch.linalg.norm(uc - 2.25 * ux + 0.5 * uy).item()
         den = torch.linalg.norm(ux).item() + torch.linalg.norm(uy).item()
         assert num <= 1e-12 * den
+
+
+def simulate_subtree_split(G, tree, w_np, nranks):
+    """All nranks of the subtree-split evaluation on ONE device: stage1 per rank, the all-gather
+    as a concatenation of the send buffers, stage2 per rank (each writes its own rows of u)."""
+    import torch
+
+    r = w_np.shape[1]
+    evs = [G.Evaluator(tree, rank=g, nranks=nranks) for g in range(nranks)]
+    infos = [e.dist_info() for e in evs]
+    slot = infos[0]["max_send_rows"] * r
+    w = torch.from_numpy(np.ascontiguousarray(w_np.T)).cuda().t()
+    sends = [torch.zeros(slot, dtype=torch.float64, device="cuda") for _ in evs]
+    for e, sb in zip(evs, sends):
+        e.dist_stage1_torch(w, sb)
+    recv = torch.cat(sends) if slot else torch.zeros(0, dtype=torch.float64, device="cuda")
+    u = torch.full((r, tree.n), float("nan"), dtype=torch.float64, device="cuda").t()
+    for e in evs:
+        e.dist_stage2_torch(recv, r, u)
+    torch.cuda.synchronize()
+    out = u.cpu().numpy()
+    for e in evs:
+        e.close()
+    return out, infos
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 4, 8])
+def test_subtree_split_matches_single_gpu(gpu, oracle, nranks):
+    """north_star (4): subtree split + one all-gather reproduces the single-GPU / reference result."""
+    from paper_1707_00164_b200 import synth
+
+    tree, _ = synth.make_config_tree("c3", n=1 << 15, seed=1)
+    w = np.asfortranarray(np.random.default_rng(5).standard_normal((tree.n, 24)))
+    with gpu.Evaluator(tree) as ev:
+        single = ev.evaluate(w)
+    u, infos = simulate_subtree_split(gpu, tree, w, nranks)
+    assert not np.isnan(u).any(), "some rows of u were not written by their owner"
+    assert rel2(u, single.u) <= TOL
+    assert all(i["full_flops_per_rhs"] * 24 == single.flops for i in infos)
+    assert sum(i["own_row_end"] - i["own_row_begin"] for i in infos) == tree.n
+
+
+def test_subtree_split_reference_tree(gpu, oracle):
+    """Same on a tree from the reference compress (acceptance fixture, N=4096, 4 ranks) vs the oracle."""
+    pc = oracle.points_gaussian(4096, 6, 42)
+    h = oracle.compress_kernel(oracle.GAUSSIAN, pc, 1.0, m=256, s=256, kind=oracle.ANGLE, seed=42, threads=8)
+    tree = to_tree(h.export())
+    w = oracle.rng_gauss(4096, 8, 2)
+    u_ref, _, _ = h.evaluate(w)
+    u, _ = simulate_subtree_split(gpu, tree, w, 4)
+    assert rel2(u, u_ref) <= TOL
