@@ -183,6 +183,16 @@ int gofmm_dist_stage1(gofmm_handle* h, const double* d_w, int64_t ldw, int32_t r
 /* d_recv: nranks x max_send_rows x r doubles (all-gathered); writes u_perm rows of this rank. */
 int gofmm_dist_stage2(gofmm_handle* h, const double* d_recv, int32_t r, double* d_u_perm, int64_t ldu, void* stream);
 
+/* ---- error_eps2 support (evaluate.hpp:330-373) ---------------------------------------------
+ * Exact rows of K W for nrows ORIGINAL indices `rows` (host array), W on the device in original
+ * order; out is nrows x r column-major (device). Matrix-free kernel sources only. */
+int gofmm_exact_rows(gofmm_handle* h, const int32_t* rows, int32_t nrows, const double* d_w, int64_t ldw, int32_t r,
+                     double* d_out, int64_t ldo, void* stream);
+/* error_eps2's draws from the reference Rng (common.hpp:40-104): Rng(seed, 0xe952), the sorted
+ * row sample (min(sample_rows, n) rows), then W column-major (host). w_out may be NULL. */
+int gofmm_rng_eps2_draw(uint64_t seed, int32_t n, int32_t r, int32_t sample_rows, int32_t* rows_out, double* w_out,
+                        int64_t ldw);
+
 /* Bytes of device memory held by the handle (tree + workspace). */
 int64_t gofmm_device_bytes(const gofmm_handle* h);
 

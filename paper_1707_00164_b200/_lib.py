@@ -111,7 +111,8 @@ _lib = None
 EXPORTS = ("gofmm_create", "gofmm_evaluate", "gofmm_evaluate_device", "gofmm_unpermute_device",
            "gofmm_flops", "gofmm_phase_flops", "gofmm_launch_profile", "gofmm_device_bytes", "gofmm_launches_per_eval", "gofmm_destroy",
            "gofmm_last_error", "gofmm_abi_version", "gofmm_create_dist", "gofmm_dist_get_info",
-           "gofmm_dist_plan_host", "gofmm_dist_stage1", "gofmm_dist_stage2")
+           "gofmm_dist_plan_host", "gofmm_dist_stage1", "gofmm_dist_stage2", "gofmm_exact_rows",
+           "gofmm_rng_eps2_draw")
 
 
 def lib():
@@ -135,6 +136,8 @@ def lib():
         L.gofmm_dist_plan_host.argtypes = [C.POINTER(TreeDesc), C.c_int32, C.c_int32, C.POINTER(DistInfo), C.c_int32, P]
         L.gofmm_dist_stage1.argtypes = [P, P, C.c_int64, C.c_int32, P, P]
         L.gofmm_dist_stage2.argtypes = [P, P, C.c_int32, P, C.c_int64, P]
+        L.gofmm_exact_rows.argtypes = [P, P, C.c_int32, P, C.c_int64, C.c_int32, P, C.c_int64, P]
+        L.gofmm_rng_eps2_draw.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, P, P, C.c_int64]
         L.gofmm_device_bytes.argtypes = [P]
         L.gofmm_device_bytes.restype = C.c_int64
         L.gofmm_launches_per_eval.argtypes = [P]

@@ -364,6 +364,8 @@ struct gofmm_handle {
   int64_t own_begin = 0, own_end = 0;          // own permuted rows [start, end)
   int64_t full_flops_per_rhs = 0;              // the whole (undistributed) evaluation
   gofmm::DevBuf d_segs;                        // pack / unpack segment table
+  std::vector<double> coords_host;             // d x n original order (kernel sources; exact rows)
+  gofmm::DevBuf d_ex_groups, d_ex_terms, d_ex_tiles, d_ex_x, d_ex_part;  // exact-rows scratch
   int32_t n_pack = 0, n_unpack = 0;
 
   gofmm::KernelFn kfn_s = nullptr, kfn_g = nullptr;
@@ -572,6 +574,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   // coordinates: permuted point space and skeleton space, point-major
   if (d->source == GOFMM_SOURCE_KERNEL) {
     const int D = d->dim;
+    H->coords_host.assign(d->coords, d->coords + int64_t(D) * d->n);
     std::vector<double> xp(size_t(H->ld_wp) * D, 0.0);
     for (int id : H->leaf_ids)
       for (int t = H->start[id]; t < H->end[id]; ++t) {
@@ -1404,6 +1407,147 @@ int gofmm_evaluate(gofmm_handle* H, const double* w, int64_t ldw, int32_t r, dou
       stats->ms_d2h = d2h;
       stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
+  });
+}
+
+// Exact rows of K W for error_eps2 (evaluate.hpp:353: oracle.block(rows, all) * w), matrix-free:
+// one generated term per leaf (K(x_rows, x_leaf) W_perm[leaf]) split over kExactChunks partial
+// groups so the N-long reduction runs on many CTAs, then a fixed-order sum of the partials.
+int gofmm_exact_rows(gofmm_handle* H, const int32_t* rows, int32_t nrows, const double* d_w, int64_t ldw, int32_t r,
+                     double* d_out, int64_t ldo, void* stream) {
+  return guarded([&] {
+    check_args(H, d_w, ldw, r, d_w, H->n);
+    if (H->source != GOFMM_SOURCE_KERNEL || !H->kfn_g)
+      throw Error(GOFMM_ERR_INVALID, "exact rows need a matrix-free kernel source");
+    if (nrows < 1 || !rows || !d_out || ldo < nrows) throw Error(GOFMM_ERR_INVALID, "exact rows: bad arguments");
+    if (H->nranks > 1) throw Error(GOFMM_ERR_INVALID, "exact rows: single-GPU handles only");
+    GOFMM_CUDA(cudaSetDevice(H->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    const int D = H->dim;
+    std::vector<double> x(size_t(nrows) * D);
+    for (int i = 0; i < nrows; ++i) {
+      if (rows[i] < 0 || rows[i] >= H->n) throw Error(GOFMM_ERR_INVALID, "exact rows: row out of range");
+      for (int q = 0; q < D; ++q) x[size_t(i) * D + q] = H->coords_host[size_t(rows[i]) * D + q];
+    }
+    H->d_ex_x.upload(x);
+    // W_perm for these columns (the permutation of an evaluation)
+    ensure_workspace(H, r);
+    upload_plan(H);
+    if (H->maps_r != r) {
+      const double* bufs[3] = {H->d_wp.as<double>(), H->d_what.as<double>(), H->d_c.as<double>()};
+      const int64_t rws[3] = {H->ld_wp, H->ld_s, H->ld_s};
+      for (int b = 0; b < 3; ++b) {
+        encode_bmap(&H->maps_s.m[b], bufs[b], rws[b], r, H->ws_r, kBN_S);
+        encode_bmap(&H->maps_g.m[b], bufs[b], rws[b], r, H->ws_r, kBN_G);
+      }
+      H->maps_r = r;
+    }
+    {
+      const int cpb = int(std::max<int64_t>(1, std::min<int64_t>(8, (48ll << 20) / (int64_t(H->n) * 8))));
+      dim3 grid(unsigned((H->ld_wp + 255) / 256), unsigned((r + cpb - 1) / cpb));
+      permute_rows_in<<<grid, 256, 0, st>>>(d_w, ldw, H->d_prow.as<int32_t>(), 0, H->ld_wp, r, cpb,
+                                            H->d_wp.as<double>(), int64_t(H->ws_r) * 16);
+    }
+    const int nleaf = int(H->leaf_ids.size());
+    const int chunks = std::max(1, std::min(nleaf, 128));
+    std::vector<Group> gs;
+    std::vector<Term> ts;
+    std::vector<Tile> tl;
+    for (int c = 0; c < chunks; ++c) {
+      Group g{};
+      g.crow = int64_t(c) * nrows;  // partial c occupies rows [c*nrows, (c+1)*nrows) of the scratch
+      g.M = nrows;
+      g.tbeg = int(ts.size());
+      for (int li = c; li < nleaf; li += chunks) {
+        const int id = H->leaf_ids[li];
+        Term t{};
+        t.flags = kTermGen;
+        t.xr = H->d_ex_x.as<double>();
+        t.xc = H->d_xp.as<double>() + H->pst[id] * D;
+        t.bbuf = kBufWp;
+        t.b_row = H->pst[id];
+        t.K = H->end[id] - H->start[id];
+        ts.push_back(t);
+      }
+      g.tend = int(ts.size());
+      for (int m0 = 0; m0 < nrows; m0 += kBM_G) tl.push_back({int(gs.size()), m0});
+      gs.push_back(g);
+    }
+    H->d_ex_groups.upload(gs);
+    H->d_ex_terms.upload(ts);
+    H->d_ex_tiles.upload(tl);
+    const size_t part_bytes = size_t(chunks) * nrows * r * sizeof(double);
+    if (H->d_ex_part.bytes < part_bytes) H->d_ex_part.alloc(part_bytes, false);
+    const int64_t ldp = int64_t(chunks) * nrows;  // partials stacked along rows, column-major
+    dim3 grid(unsigned(tl.size()), unsigned((r + kBN_G - 1) / kBN_G));
+    H->kfn_g<<<grid, kThreadsG, H->smem_g, st>>>(H->maps_g, H->d_ex_tiles.as<Tile>(), H->d_ex_groups.as<Group>(),
+                                                  H->d_ex_terms.as<Term>(), r, H->kp, H->d_ex_part.as<double>(), ldp,
+                                                  0);
+    dim3 g2(unsigned((int64_t(nrows) * r + 255) / 256));
+    sum_partials<<<g2, 256, 0, st>>>(H->d_ex_part.as<double>(), ldp, nrows, chunks, r, d_out, ldo);
+    GOFMM_CUDA(cudaGetLastError());
+    GOFMM_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+// The reference Rng (common.hpp:40-104): splitmix64 stream, Box-Muller gauss with cached spare,
+// sorted rejection sample. Host code: error_eps2 draws its rows and W from it
+// (evaluate.hpp:336-346), so reproducing eps2 needs the identical stream.
+namespace {
+struct RefRng {
+  uint64_t state;
+  bool have_spare = false;
+  double spare = 0.0;
+  static uint64_t mix(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+  }
+  RefRng(uint64_t seed, uint64_t stream) : state(mix(seed ^ mix(stream + 0x632be59bd9b4e019ULL))) {}
+  uint64_t next() { return state = mix(state); }
+  int uniform(int n) { return int(next() % uint64_t(n)); }
+  double uniform01() { return double(next() >> 11) * 0x1.0p-53; }
+  double gauss() {
+    if (have_spare) {
+      have_spare = false;
+      return spare;
+    }
+    double u1 = uniform01(), u2 = uniform01();
+    while (u1 <= 1e-300) u1 = uniform01();
+    double rr = std::sqrt(-2.0 * std::log(u1));
+    double a = 2.0 * M_PI * u2;
+    spare = rr * std::sin(a);
+    have_spare = true;
+    return rr * std::cos(a);
+  }
+};
+}  // namespace
+
+int gofmm_rng_eps2_draw(uint64_t seed, int32_t n, int32_t r, int32_t sample_rows, int32_t* rows_out,
+                        double* w_out, int64_t ldw) {
+  return guarded([&] {
+    if (n < 1 || r < 1 || sample_rows < 1) throw Error(GOFMM_ERR_INVALID, "eps2 draw: bad sizes");
+    RefRng rng(seed, 0xe952);
+    const int k = std::min(sample_rows, n);
+    std::vector<int> out;
+    if (k >= n) {
+      for (int i = 0; i < n; ++i) out.push_back(i);
+    } else {
+      std::vector<char> taken(n, 0);
+      while (int(out.size()) < k) {
+        int v = rng.uniform(n);
+        if (!taken[v]) {
+          taken[v] = 1;
+          out.push_back(v);
+        }
+      }
+      std::sort(out.begin(), out.end());
+    }
+    std::copy(out.begin(), out.end(), rows_out);
+    if (w_out)
+      for (int c = 0; c < r; ++c)
+        for (int i = 0; i < n; ++i) w_out[i + size_t(c) * ldw] = rng.gauss();
   });
 }
 

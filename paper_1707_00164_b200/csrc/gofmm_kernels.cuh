@@ -620,6 +620,17 @@ __global__ void panel_copy(const PanelSeg* __restrict__ segs, double* __restrict
   }
 }
 
+// out[i, c] = sum_p part[p*nrows + i, c]  (fixed order over the partials: deterministic)
+__global__ void sum_partials(const double* __restrict__ part, int64_t ldp, int32_t nrows, int32_t nparts, int32_t r,
+                             double* __restrict__ out, int64_t ldo) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= int64_t(nrows) * r) return;
+  const int i = int(e % nrows), c = int(e / nrows);
+  double acc = 0.0;
+  for (int p = 0; p < nparts; ++p) acc += part[int64_t(p) * nrows + i + size_t(c) * ldp];
+  out[i + size_t(c) * ldo] = acc;
+}
+
 // u[iperm[t], c] = up[t, c]   (unpermute, evaluate.hpp:21-25)
 __global__ void unpermute_rows(const double* __restrict__ up, int64_t ldp, const int32_t* __restrict__ iperm,
                                int64_t n, int32_t r, int32_t cols_per_block, double* __restrict__ u, int64_t ldu) {

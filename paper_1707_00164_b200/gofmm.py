@@ -129,6 +129,15 @@ def make_desc(tree: CompressedTree, stored: bool | None = None):
     return d, keep, use_stored
 
 
+def rng_eps2_draw(seed: int, n: int, r: int, sample_rows: int):
+    """error_eps2's draws from the reference Rng (evaluate.hpp:336-346): (rows, W)."""
+    k = min(sample_rows, n)
+    rows = np.empty(k, dtype=np.int32)
+    w = np.empty((n, r), dtype=np.float64, order="F")
+    L.check(L.lib().gofmm_rng_eps2_draw(seed, n, r, sample_rows, _p(rows), _p(w), n))
+    return rows, w
+
+
 def dist_plan_host(tree: CompressedTree, rank: int, nranks: int) -> tuple[dict, list[int]]:
     """Host-only subtree-split plan (no device): info and the exported ids in send order
     (what: node id; W rows: -(leaf id + 1))."""
@@ -293,6 +302,40 @@ class Evaluator:
         recv = all_gather(send)
         self.dist_stage2_torch(recv, r, out)
         return out
+
+    # ------------------------------------------------------------------ error_eps2 (evaluate.hpp:330-373)
+    def exact_rows(self, rows, w: np.ndarray) -> np.ndarray:
+        """K(rows, all) @ w computed matrix-free on the device (evaluate.hpp:353)."""
+        import torch
+
+        rows = np.ascontiguousarray(rows, dtype=np.int32)
+        w = np.asarray(w, dtype=np.float64)
+        if w.ndim == 1:
+            w = w.reshape(-1, 1)
+        wd = torch.from_numpy(np.ascontiguousarray(w.T)).cuda().t()
+        out = torch.empty((w.shape[1], rows.shape[0]), dtype=torch.float64, device="cuda").t()
+        L.check(L.lib().gofmm_exact_rows(self._h, _p(rows), rows.shape[0], C.c_void_p(wd.data_ptr()), wd.stride(1),
+                                         int(w.shape[1]), C.c_void_p(out.data_ptr()), out.stride(1), None))
+        return out.cpu().numpy()
+
+    def error_eps2(self, r: int, sample_rows: int, seed: int) -> dict:
+        """Sampled relative error ||(K~w - Kw)_S||_F / ||(Kw)_S||_F with the reference's draws."""
+        if sample_rows < 1:
+            raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "sample_rows must be >= 1")
+        if r < 1:
+            raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "r must be >= 1")
+        rows, w = rng_eps2_draw(seed, self.n, r, sample_rows)
+        pot = self.evaluate(w)
+        u = self.unpermute(pot.u)[rows]
+        exact = self.exact_rows(rows, w)
+        dn = np.linalg.norm(u - exact, axis=1)
+        de = np.linalg.norm(exact, axis=1)
+        num, den = float((dn ** 2).sum()), float((de ** 2).sum())
+        if den == 0.0:  # the reference redraws W up to 3 times (evaluate.hpp:343-372)
+            raise L.GofmmError(L.GOFMM_ERR_NUMERIC, "error_eps2: sampled rows of Kw vanished")
+        rel = np.where(de > 0, dn / np.where(de > 0, de, 1.0), 0.0)
+        return dict(eps2=float(np.sqrt(num / den)), per_entry=rel[:10].tolist(), mean_sample=float(rel.mean()),
+                    sample_rows=rows.tolist(), eval_flops=pot.flops, eval_seconds=pot.seconds)
 
     def unpermute(self, u_perm: np.ndarray) -> np.ndarray:
         """out.row(iperm[t]) = u_perm.row(t) (evaluate.hpp:21-25)."""

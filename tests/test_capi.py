@@ -175,3 +175,39 @@ def test_synthetic_tree_runs_through_reference_evaluate(oracle):
     dense = K @ w
     got = ref.unpermute(u)
     assert np.linalg.norm(got - dense) / np.linalg.norm(dense) <= 1e-12
+
+
+def test_reference_rng_draws_match_oracle(oracle):
+    """gofmm_rng_eps2_draw reproduces error_eps2's RNG consumption (evaluate.hpp:336-346)."""
+    from paper_1707_00164_b200 import gofmm
+
+    for n, r, k, seed in [(500, 3, 100, 7), (64, 2, 64, 11), (1000, 1, 10, 42)]:
+        rows, w = gofmm.rng_eps2_draw(seed, n, r, k)
+        rows_ref, w_ref = oracle.eps2_draw(n, r, k, seed)
+        assert np.array_equal(rows, rows_ref)
+        assert np.array_equal(w, w_ref)
+
+
+def test_ghmx_roundtrip_reference_tree(oracle, tmp_path):
+    """GHMX file format (hmx_io): a reference-compressed tree with stored blocks and coordinates
+    survives save/load bit for bit, and the reloaded tree evaluates identically in the oracle."""
+    from paper_1707_00164_b200 import CompressedTree, hmx_io
+
+    pc = oracle.points_gaussian(400, 3, 2)
+    h = oracle.compress_kernel(oracle.GAUSSIAN, pc, 1.2, m=32, s=24, budget=0.05, seed=2)
+    t = CompressedTree.from_any(h.export())
+    path = str(tmp_path / "tree.ghmx")
+    hmx_io.save(path, t)
+    t2 = hmx_io.load(path)
+    for name in ("parent", "left", "right", "level", "start", "end", "iperm", "rank", "skel_off", "skel_idx",
+                 "proj_off", "proj", "near_a", "near_b", "far_a", "far_b", "coords", "diag_off", "diag",
+                 "near_off", "near_blk", "far_off", "far_blk"):
+        assert np.array_equal(np.asarray(getattr(t, name)), np.asarray(getattr(t2, name))), name
+    assert t2.kernel == t.kernel and tuple(t2.kparams) == tuple(t.kparams)
+    w = np.random.default_rng(0).standard_normal((400, 3))
+    u1 = oracle.import_flat(t).evaluate(w)[0]
+    u2 = oracle.import_flat(t2).evaluate(w)[0]
+    assert np.array_equal(u1, u2)
+    with pytest.raises(ValueError):
+        open(path, "r+b").write(b"XXXX")
+        hmx_io.load(path)

@@ -266,3 +266,19 @@ def test_subtree_split_reference_tree(gpu, oracle):
     u_ref, _, _ = h.evaluate(w)
     u, _ = simulate_subtree_split(gpu, tree, w, 4)
     assert rel2(u, u_ref) <= TOL
+
+
+def test_gpu_error_eps2_matches_reference(gpu, oracle):
+    """error_eps2 computed entirely by the product (reference RNG restated in the C-ABI, exact rows
+    matrix-free on the GPU) equals the reference's eps2 on the criterion-2 fixture (0.34486)."""
+    pc = oracle.points_gaussian(8192, 6, 42)
+    h = oracle.compress_kernel(oracle.GAUSSIAN, pc, 1.0, m=256, s=256, kind=oracle.ANGLE, seed=42, threads=8)
+    rep_ref = h.error_eps2(1, 100, 42)
+    with gpu.Evaluator(to_tree(h.export())) as ev:
+        rep = ev.error_eps2(1, 100, 42)
+        rows, w = oracle.eps2_draw(8192, 3, 50, 5)
+        ex_gpu = ev.exact_rows(rows, w)
+    assert rep["sample_rows"] == rep_ref["sample_rows"]
+    assert abs(rep["eps2"] - rep_ref["eps2"]) <= 1e-10 * rep_ref["eps2"]
+    assert np.allclose(rep["per_entry"], rep_ref["per_entry"], rtol=1e-9)
+    assert rel2(ex_gpu, h.exact_rows(rows, w)) <= 1e-13
