@@ -33,6 +33,26 @@ FP64_PEAK_FILE = os.path.join(HERE, "profiles", "r01_fp64_peak.json")
 NCU_SUMMARY_FILE = os.path.join(HERE, "profiles", "r01_ncu_summary.json")
 
 
+def tf32x3_peak_tflops() -> tuple[float, str]:
+    """Peak for the FP32 path: 3xTF32 issues three TF32 tensor-core MMAs per algorithmic product,
+    so the algorithmic ceiling is the dense TF32 peak / 3. Dense TF32 = half the dense bf16 rate:
+    from MEASURED_PEAKS.json (driver-written cuBLAS bf16) when present, else the 1.1 PF/s nominal of
+    /opt/skills/guides/B200_PROFILING.md."""
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        for k, v in d.items():
+            if "bf16" in k.lower() and isinstance(v, (int, float)) and v > 100:
+                tf = float(v) / 2.0  # TF/s
+                return tf / 3.0, f"MEASURED_PEAKS.json {k}={v} -> tf32 dense {tf:.0f} TF/s, / 3 (3xTF32)"
+    except Exception:
+        pass
+    return 1100.0 / 3.0, "nominal tf32 dense 1.1 PF/s (B200_PROFILING.md) / 3 (3xTF32)"
+
+
+FP32_SIMT_PEAK = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4 TF/s: FFMA peak, for context
+
+
 def fp64_peak_tflops() -> tuple[float, str]:
     """Measured FP64 DMMA peak of this pool's B200 (MEASURED_PEAKS.json has no FP64 entry)."""
     try:
@@ -209,22 +229,25 @@ def ours_arm(args, world, rank, local):
     tree, cfg = synth.make_config_tree(args.config, seed=args.seed,
                                        **{k: cfg[k] for k in ("n", "budget")})
     t_gen = time.perf_counter() - t0
+    f32 = args.precision == "fp32"
+    tdt = torch.float32 if f32 else torch.float64
+    esz = 4 if f32 else 8
     t0 = time.perf_counter()
-    ev = Evaluator(tree, device=local)
+    ev = Evaluator(tree, device=local, precision=args.precision)
     t_create = time.perf_counter() - t0
     flops = ev.flops(r)
     pflops = ev.phase_flops(r)
 
     gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
-    w = torch.randn((r, tree.n), dtype=torch.float64, device="cuda", generator=gen).t()  # N x r column-major
-    u = torch.empty((r, tree.n), dtype=torch.float64, device="cuda").t()
+    w = torch.randn((r, tree.n), dtype=tdt, device="cuda", generator=gen).t()  # N x r column-major
+    u = torch.empty((r, tree.n), dtype=tdt, device="cuda").t()
     for _ in range(args.warmup):
         ev.evaluate_torch(w, out=u)
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
     # inputs smaller than 2x L2 (126 MB): flush L2 between steps (outside the per-step events)
-    small = tree.n * r * 8 < 2 * 126 * 2 ** 20
+    small = tree.n * r * esz < 2 * 126 * 2 ** 20
     flush = torch.empty(256 * 2 ** 20 // 8, dtype=torch.float64, device="cuda") if small else None
     with ClockSampler(local) as clk:
         barrier(world)
@@ -255,20 +278,22 @@ def ours_arm(args, world, rank, local):
     # kernels are launched on); the roofline reports the longest single launch
     _, ph = ev.evaluate_torch(w, out=u, sync_stats=True)
     torch.cuda.synchronize()
-    peak, peak_src = fp64_peak_tflops()
+    peak, peak_src = tf32x3_peak_tflops() if f32 else fp64_peak_tflops()
     phases = {"upward": (pflops["upward"], ph["ms_upward"]), "downward": (pflops["downward"], ph["ms_downward"]),
               "output": (pflops["output"], ph["ms_output"])}
     launches = ev.launch_profile(r)
     dom = max(launches, key=lambda x: x["ms"])
     achieved = dom["flops"] / (dom["ms"] * 1e-3) / 1e12 if dom["ms"] > 0 else 0.0
-    dom_name = f"grouped_gemm_f64 {dom['phase']} launch (level {dom['level']})" if dom["level"] >= 0 else \
-        "grouped_gemm_f64 output launch (L2L + leaf S2N)"
+    kname = "grouped_gemm_tf32x3" if f32 else "grouped_gemm_f64"
+    dom_name = f"{kname} {dom['phase']} launch (level {dom['level']})" if dom["level"] >= 0 else \
+        f"{kname} output launch (L2L + leaf S2N)"
     traffic = None
     try:
         with open(NCU_SUMMARY_FILE) as f:
             nsum = json.load(f)
         for rec in nsum.get("launches", []):
             if (rec.get("config") == args.config and rec.get("phase") == dom["phase"]
+                    and rec.get("precision", "fp64") == args.precision
                     and rec.get("level") == dom["level"] and rec.get("n") == tree.n and rec.get("r") == r):
                 traffic = rec.get("dram_bytes")
     except Exception:
@@ -277,9 +302,9 @@ def ours_arm(args, world, rank, local):
     # end-to-end through the host API (pinned host W and u; H2D + D2H inside the timed region)
     e2e = None
     if not args.no_e2e:
-        w_h = torch.empty((r, tree.n), dtype=torch.float64, pin_memory=True)
+        w_h = torch.empty((r, tree.n), dtype=tdt, pin_memory=True)
         w_h.copy_(w.t())
-        u_h = torch.empty((r, tree.n), dtype=torch.float64, pin_memory=True)
+        u_h = torch.empty((r, tree.n), dtype=tdt, pin_memory=True)
         wn, un = w_h.numpy().T, u_h.numpy().T  # Fortran-ordered N x r views of pinned memory
         ev.evaluate(wn, out=un)  # warm
         barrier(world)
@@ -291,7 +316,7 @@ def ours_arm(args, world, rank, local):
         barrier(world)
         sec = allmax(float(np.mean(ts)), world)
         e2e = {"value": round(world * flops / sec / 1e9, 3), "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(tree.n * r * 8), "d2h_bytes_per_step": int(tree.n * r * 8),
+               "h2d_bytes_per_step": int(tree.n * r * esz), "d2h_bytes_per_step": int(tree.n * r * esz),
                "sec_per_eval": round(sec, 5), "ms_h2d": round(p.stats["ms_h2d"], 3),
                "ms_d2h": round(p.stats["ms_d2h"], 3)}
         del w_h, u_h
@@ -311,9 +336,9 @@ def ours_arm(args, world, rank, local):
                    "kind": "reference",
                    "sample": f"{args.config}-shaped tree at N={stree.n} (same d/m/s/budget/kernel), r={r}, "
                              f"reference gfmm::evaluate TaskDag x{threads} threads, median of 2 Potentials.seconds"}
-            with Evaluator(stree, device=local) as es:
+            with Evaluator(stree, device=local, precision=args.precision) as es:
                 pu = es.evaluate(res["w"])
-            rel_err = float(np.linalg.norm(pu.u - res["u"]) / np.linalg.norm(res["u"]))
+            rel_err = float(np.linalg.norm(pu.u.astype(np.float64) - res["u"]) / np.linalg.norm(res["u"]))
         except Exception as exc:  # report, never hide
             cpu = {"value": None, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {exc!r}"[:300]}
@@ -321,16 +346,17 @@ def ours_arm(args, world, rank, local):
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f32" if f32 else "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {KERNEL_NAMES.get(cfg['kernel'], 'kernel')} h={cfg['h']} N={tree.n} "
                                f"d={cfg['d']} m={cfg['m']} "
                                f"s={cfg['s']} budget={cfg['budget']} r={r} per GPU", "n": tree.n, "d": cfg["d"],
                    "m": cfg["m"], "s": cfg["s"], "budget": cfg["budget"], "r_per_gpu": r,
                    "near_pairs": int(len(tree.near_a)), "far_pairs": int(len(tree.far_a)),
-                   "tree": "synthetic saturated-rank tree (synth.py)", "l2_flush": (f"L2 flushed between steps (256 MB write, outside the per-step events); W {tree.n * r * 8 / 1e6:.1f} MB" if small else f"inputs larger than L2 (W {tree.n * r * 8 / 1e9:.2f} GB)"),
-                   "parallelism": "single GPU"},
+                   "tree": "synthetic saturated-rank tree (synth.py)", "l2_flush": (f"L2 flushed between steps (256 MB write, outside the per-step events); W {tree.n * r * esz / 1e6:.1f} MB" if small else f"inputs larger than L2 (W {tree.n * r * esz / 1e9:.2f} GB)"),
+                   "parallelism": "single GPU", "precision": args.precision,
+                   "arithmetic": "3xTF32 on tcgen05 (FP32 accumulate in TMEM)" if f32 else "FP64 DMMA"},
         "sec_per_eval": round(ms / 1e3, 6),
-        "pct_fp64_peak": round(100.0 * value / 1e3 / (peak * world), 2),
+        ("pct_3xtf32_peak" if f32 else "pct_fp64_peak"): round(100.0 * value / 1e3 / (peak * world), 2),
         "flops_per_eval": int(flops),
         "rel_error": rel_err,
         "phase_ms": {k: round(v[1], 3) for k, v in phases.items()} | {"permute": round(ph["ms_permute"], 3)},
@@ -343,6 +369,9 @@ def ours_arm(args, world, rank, local):
         "gpu_launches": int(ev.launches_per_eval * args.steps),
         "setup_s": {"tree_gen": round(t_gen, 2), "create_upload": round(t_create, 2)},
     }
+    if f32:
+        line["pct_fp32_simt_peak"] = round(100.0 * value / 1e3 / (FP32_SIMT_PEAK * world), 2)
+        line["tolerance"] = "rel. 2-norm 1e-5 vs the reference FP64 evaluate (north_star, fp32)"
     if rank == 0:
         line["clocks"] = clk.summary()
         print(json.dumps(line), flush=True)
@@ -459,6 +488,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
     ap.add_argument("--budget", type=float, default=None)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--r", type=int, default=None)
@@ -474,6 +504,8 @@ def main():
     if args.impl == "reference":
         rc = reference_arm(args, world, rank)
     elif world > 1 or args.dist:
+        if args.precision != "fp64":
+            raise SystemExit("the subtree-split (multi-GPU) path is fp64 only")
         rc = dist_arm(args, world, rank, local)
     else:
         rc = ours_arm(args, world, rank, local)

@@ -47,6 +47,14 @@ extern "C" {
 #define GOFMM_KERNEL_POLYNOMIAL 2  /* (xi.xj + c)^p                     oracle.hpp:208-218, kparam={c,p} */
 #define GOFMM_KERNEL_EXPONENTIAL 4 /* exp(-|xi-xj| * (1/h))             Matern-1/2, kparam[0]=h */
 
+/* Arithmetic precision of a handle (gofmm_options.precision). The reference computes in FP64
+ * only (common.hpp:18, Matrix = Eigen::MatrixXd); FP32 is north_star's second tolerance class
+ * (relative 2-norm error 1e-5 vs the reference), computed as 3xTF32 on the tcgen05 tensor cores.
+ * An FP32 handle is evaluated with the *_f32 entry points, an FP64 handle with the others;
+ * mixing them fails with GOFMM_ERR_INVALID. */
+#define GOFMM_PRECISION_F64 0
+#define GOFMM_PRECISION_F32 1
+
 /* Block materialisation modes (GOFMM_SOURCE_KERNEL only). */
 #define GOFMM_BLOCKS_MATRIX_FREE 0 /* regenerate K entries inside the tile GEMM (never stored) */
 #define GOFMM_BLOCKS_MATERIALIZE 1 /* generate once on device at create, keep in HBM */
@@ -99,6 +107,7 @@ typedef struct gofmm_options {
   int32_t near_mode;  /* GOFMM_BLOCKS_* for D and near (S) blocks; default matrix-free */
   int32_t far_mode;   /* GOFMM_BLOCKS_* for far (coupling) blocks */
   int32_t max_rhs_chunk; /* columns per internal pass; 0 = as many as fit in free HBM */
+  int32_t precision;     /* GOFMM_PRECISION_* (default FP64) */
 } gofmm_options;
 
 typedef struct gofmm_eval_stats {
@@ -125,6 +134,18 @@ int gofmm_evaluate(gofmm_handle* h, const double* w, int64_t ldw, int32_t r, dou
  * returns; stats->flops is filled, the phase times are filled only when stats_sync != 0. */
 int gofmm_evaluate_device(gofmm_handle* h, const double* d_w, int64_t ldw, int32_t r, double* d_u_perm,
                           int64_t ldu, void* stream, int32_t stats_sync, gofmm_eval_stats* stats);
+
+/* FP32 variants (handles created with precision GOFMM_PRECISION_F32): same semantics, float
+ * buffers. Single-GPU handles only. */
+int gofmm_evaluate_f32(gofmm_handle* h, const float* w, int64_t ldw, int32_t r, float* u_perm, int64_t ldu,
+                       gofmm_eval_stats* stats);
+int gofmm_evaluate_device_f32(gofmm_handle* h, const float* d_w, int64_t ldw, int32_t r, float* d_u_perm,
+                              int64_t ldu, void* stream, int32_t stats_sync, gofmm_eval_stats* stats);
+int gofmm_unpermute_device_f32(gofmm_handle* h, const float* d_u_perm, int64_t ldp, int32_t r, float* d_u,
+                               int64_t ldu, void* stream);
+
+/* Precision the handle was created with (GOFMM_PRECISION_*), -1 for a null handle. */
+int32_t gofmm_precision(const gofmm_handle* h);
 
 /* unpermute (evaluate.hpp:21-25) on device: u[iperm[t], :] = u_perm[t, :]. */
 int gofmm_unpermute_device(gofmm_handle* h, const double* d_u_perm, int64_t ldp, int32_t r, double* d_u,

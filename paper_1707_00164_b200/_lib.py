@@ -28,11 +28,16 @@ KERNEL_GAUSSIAN = 0
 KERNEL_LAPLACE = 1
 KERNEL_POLYNOMIAL = 2
 KERNEL_EXPONENTIAL = 4
+PRECISION_F64 = 0
+PRECISION_F32 = 1
 BLOCKS_MATRIX_FREE = 0
 BLOCKS_MATERIALIZE = 1
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared"]
+              "-Xcompiler", "-fPIC"]
+# translation units of the library, compiled in parallel then linked: the C-ABI + FP64 DMMA
+# kernels, and the FP32 3xTF32 tcgen05 kernels
+UNITS = ("gofmm_capi.cu", "gofmm_f32.cu")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -43,11 +48,25 @@ def build(force: bool = False, verbose: bool = False) -> str:
         newest = max(os.path.getmtime(s) for s in srcs)
         if os.path.getmtime(LIB_PATH) >= newest:
             return LIB_PATH
-    os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, os.path.join(CSRC, "gofmm_capi.cu")]
+    out_dir = os.path.dirname(LIB_PATH)
+    os.makedirs(out_dir, exist_ok=True)
+    objs, procs = [], []
+    for unit in UNITS:
+        obj = os.path.join(out_dir, unit.replace(".cu", ".o"))
+        cmd = ["nvcc", *NVCC_FLAGS, "-c", "-o", obj, os.path.join(CSRC, unit)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((cmd, subprocess.Popen(cmd)))
+        objs.append(obj)
+    for cmd, p in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, cmd)
+    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB_PATH, *objs]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
+    for obj in objs:
+        os.remove(obj)
     return LIB_PATH
 
 
@@ -70,7 +89,7 @@ class TreeDesc(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("near_mode", C.c_int32), ("far_mode", C.c_int32),
-                ("max_rhs_chunk", C.c_int32)]
+                ("max_rhs_chunk", C.c_int32), ("precision", C.c_int32)]
 
 
 class EvalStats(C.Structure):
@@ -112,7 +131,8 @@ EXPORTS = ("gofmm_create", "gofmm_evaluate", "gofmm_evaluate_device", "gofmm_unp
            "gofmm_flops", "gofmm_phase_flops", "gofmm_launch_profile", "gofmm_device_bytes", "gofmm_launches_per_eval", "gofmm_destroy",
            "gofmm_last_error", "gofmm_abi_version", "gofmm_create_dist", "gofmm_dist_get_info",
            "gofmm_dist_plan_host", "gofmm_dist_stage1", "gofmm_dist_stage2", "gofmm_exact_rows",
-           "gofmm_rng_eps2_draw")
+           "gofmm_rng_eps2_draw", "gofmm_evaluate_f32", "gofmm_evaluate_device_f32",
+           "gofmm_unpermute_device_f32", "gofmm_precision")
 
 
 def lib():
@@ -127,6 +147,11 @@ def lib():
         L.gofmm_evaluate_device.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, P, C.c_int32,
                                             C.POINTER(EvalStats)]
         L.gofmm_unpermute_device.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, P]
+        L.gofmm_evaluate_f32.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, C.POINTER(EvalStats)]
+        L.gofmm_evaluate_device_f32.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, P, C.c_int32,
+                                                C.POINTER(EvalStats)]
+        L.gofmm_unpermute_device_f32.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, P]
+        L.gofmm_precision.argtypes = [P]
         L.gofmm_flops.argtypes = [P, C.c_int32]
         L.gofmm_flops.restype = C.c_int64
         L.gofmm_phase_flops.argtypes = [P, C.c_int32, P]

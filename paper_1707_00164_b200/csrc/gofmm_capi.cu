@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <tuple>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -34,6 +36,7 @@
 
 #include "../../include/gofmm_b200.h"
 #include "gofmm_kernels.cuh"
+#include "gofmm_kernels_f32.cuh"
 
 namespace gofmm {
 namespace {
@@ -215,6 +218,8 @@ struct Launch {
   int level;  // tree level (output launch: -1)
   int64_t flops_per_rhs = 0;  // reference-counted flops of this launch per RHS column
   int stage = 2;  // distributed evaluation: 1 = before the all-gather (own-subtree N2S), 2 = after
+  int first_group = 0, ngroups = 0;      // groups [first_group, first_group + ngroups)
+  int first_tile32 = 0, ntiles32 = 0;    // FP32 plan: 128-row tiles of the same groups
 };
 
 // ---------------------------------------------------------------- subtree-split distribution
@@ -368,6 +373,20 @@ struct gofmm_handle {
   gofmm::DevBuf d_ex_groups, d_ex_terms, d_ex_tiles, d_ex_x, d_ex_part;  // exact-rows scratch
   int32_t n_pack = 0, n_unpack = 0;
 
+  // FP32 (3xTF32 tcgen05) plan, precision == GOFMM_PRECISION_F32: stored A operands as K-major
+  // hi / lo copies (d_a32h / d_a32l, offsets per term), FP32 coordinates, 128-row tiles, and a
+  // workspace of hi / lo panel buffers [0] = hi, [1] = lo
+  int32_t precision = GOFMM_PRECISION_F64;
+  gofmm::DevBuf d_a32h, d_a32l, d_xp32, d_xs32, d_terms32, d_tiles32;
+  std::vector<int64_t> term_a32_off, term_a32_ld;  // per plan term (flattened group order), -1 if generated
+  gofmm::DevBuf d_wp32[2], d_what32[2], d_c32[2], d_win32, d_uout32;
+  int32_t ws32_r = 0;
+  bool plan32_uploaded = false;
+  gofmm::f32::KernelParams kp32{};
+  gofmm::f32::GemmKernel k32_s, k32_g;  // stored-only / generated launches for the current bn
+  gofmm::f32::BMaps maps32{};
+  int32_t maps32_r = 0;
+
   gofmm::KernelFn kfn_s = nullptr, kfn_g = nullptr;
   size_t smem_s = 0, smem_g = 0;
   gofmm::BMaps maps_s{}, maps_g{};
@@ -408,6 +427,133 @@ void validate(const gofmm_tree_desc* d) {
     throw Error(GOFMM_ERR_INVALID, "stored source needs leaf_diag blocks");
 }
 
+
+// ---------------------------------------------------------------- FP32 plan (3xTF32 tcgen05)
+// The FP64 device tree built above is converted once: every stored-A operand a plan term reads
+// becomes a K-major FP32 hi / lo copy (split_to_kmajor; proj twice — transposed for N2S, as is
+// for S2N — and both orientations of stored near / far blocks), coordinates become FP32, and the
+// same groups are re-tiled into 128-row tiles (UMMA M = 128). The FP64 blobs are released.
+int f32_bn(int32_t r) { return r > 128 ? 256 : r > 64 ? 128 : 64; }
+
+void build_f32(gofmm_handle* H) {
+  if (H->nranks > 1) throw Error(GOFMM_ERR_INVALID, "fp32 precision: single-GPU handles only");
+  const double* blobs[4] = {H->d_proj.as<double>(), H->d_diag.as<double>(), H->d_near.as<double>(),
+                            H->d_far.as<double>()};
+  struct Key {
+    int blob;
+    int64_t off;
+    int rm, M, K;
+    bool operator<(const Key& o) const {
+      return std::tie(blob, off, rm, M, K) < std::tie(o.blob, o.off, o.rm, o.M, o.K);
+    }
+  };
+  std::map<Key, std::pair<int64_t, int64_t>> seen;
+  std::vector<f32::SplitJob> jobs;
+  int64_t total = 0;
+  H->term_a32_off.clear();
+  H->term_a32_ld.clear();
+  for (const HostGroup& g : H->groups)
+    for (const HostTerm& t : g.terms) {
+      if (t.kind != 0) {
+        H->term_a32_off.push_back(-1);
+        H->term_a32_ld.push_back(0);
+        continue;
+      }
+      const Key key{t.a_blob, t.a_off, t.row_major ? 1 : 0, g.M, t.K};
+      auto it = seen.find(key);
+      if (it == seen.end()) {
+        const int64_t ldd = (int64_t(t.K) + 3) & ~int64_t(3);  // 16-byte rows for cp.async
+        f32::SplitJob J{};
+        J.src = blobs[t.a_blob] + t.a_off;
+        J.lds = t.lda;
+        J.dst = total;
+        J.rows = g.M;
+        J.cols = t.K;
+        J.ldd = int32_t(ldd);
+        J.trans = t.row_major ? 0 : 1;
+        jobs.push_back(J);
+        it = seen.emplace(key, std::make_pair(total, ldd)).first;
+        total += int64_t(g.M) * ldd;
+      }
+      H->term_a32_off.push_back(it->second.first);
+      H->term_a32_ld.push_back(it->second.second);
+    }
+  H->d_a32h.alloc(size_t(std::max<int64_t>(total, 4)) * sizeof(float), false);
+  H->d_a32l.alloc(size_t(std::max<int64_t>(total, 4)) * sizeof(float), false);
+  if (!jobs.empty()) {
+    DevBuf d_jobs;
+    d_jobs.upload(jobs);
+    GOFMM_CUDA(f32::launch_split(d_jobs.as<f32::SplitJob>(), int(jobs.size()), H->d_a32h.as<float>(),
+                                 H->d_a32l.as<float>(), H->stream));
+    GOFMM_CUDA(cudaStreamSynchronize(H->stream));
+  }
+  if (H->source == GOFMM_SOURCE_KERNEL) {
+    const int64_t nxp = int64_t(H->ld_wp) * H->dim, nxs = int64_t(H->ld_s) * H->dim;
+    H->d_xp32.alloc(size_t(nxp) * sizeof(float), false);
+    H->d_xs32.alloc(size_t(std::max<int64_t>(nxs, 1)) * sizeof(float), false);
+    GOFMM_CUDA(f32::launch_to_f32(H->d_xp.as<double>(), nxp, H->d_xp32.as<float>(), H->stream));
+    if (H->d_xs.p) GOFMM_CUDA(f32::launch_to_f32(H->d_xs.as<double>(), nxs, H->d_xs32.as<float>(), H->stream));
+    GOFMM_CUDA(cudaStreamSynchronize(H->stream));
+  }
+  // kernel parameters: exp(x) = 2^(x log2 e) is folded into the scale (ex2.approx in the kernel)
+  constexpr double kLog2e = 1.4426950408889634;
+  H->kp32 = {};
+  H->kp32.dim = H->dim;
+  if (H->kernel == kGaussian || H->kernel == kExponential) {
+    H->kp32.p0 = float(H->kp.p0 * kLog2e);
+  } else {
+    H->kp32.p0 = float(H->kp.p0);
+    H->kp32.p1 = float(H->kp.p1);
+  }
+  // 128-row tiles of the same groups
+  std::vector<Tile> tiles32;
+  for (Launch& L : H->launches) {
+    L.first_tile32 = int(tiles32.size());
+    for (int gi = L.first_group; gi < L.first_group + L.ngroups; ++gi)
+      for (int m0 = 0; m0 < std::max(H->groups[gi].M, 0); m0 += f32::kBM) tiles32.push_back({gi, m0});
+    L.ntiles32 = int(tiles32.size()) - L.first_tile32;
+  }
+  H->d_tiles32.upload(tiles32);
+  // groups and FP32 terms do not depend on the workspace (B operands go through tensor maps)
+  std::vector<Group> gs;
+  std::vector<f32::Term> ts;
+  const float* xb[2] = {H->d_xp32.as<float>(), H->d_xs32.as<float>()};
+  const int bid[4] = {kBufWp, kBufWhat, kBufC, kBufC};
+  size_t ti = 0;
+  for (const HostGroup& hg : H->groups) {
+    Group g{};
+    g.crow = hg.c_row;
+    g.M = hg.M;
+    g.tbeg = int(ts.size());
+    for (const HostTerm& ht : hg.terms) {
+      f32::Term t{};
+      t.bbuf = bid[int(ht.b_buf)];
+      t.b_row = ht.b_row;
+      t.K = ht.K;
+      if (ht.kind == 1) {
+        t.flags = kTermGen;
+        t.xr = xb[ht.x_blob] + ht.xr_off * H->dim;
+        t.xc = xb[ht.x_blob] + ht.xc_off * H->dim;
+      } else {
+        t.a_hi = H->d_a32h.as<float>() + H->term_a32_off[ti];
+        t.a_lo = H->d_a32l.as<float>() + H->term_a32_off[ti];
+        t.lda = H->term_a32_ld[ti];
+      }
+      ts.push_back(t);
+      ++ti;
+    }
+    g.tend = int(ts.size());
+    gs.push_back(g);
+  }
+  H->d_groups.upload(gs);
+  H->d_terms32.upload(ts.empty() ? std::vector<f32::Term>(1) : ts);
+  // the FP64 operand blobs are not read by an FP32 handle
+  H->d_proj.release();
+  H->d_diag.release();
+  H->d_near.release();
+  H->d_far.release();
+}
+
 void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   const int nn = d->num_nodes;
   H->n = d->n;
@@ -419,6 +565,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     H->near_mode = o->near_mode;
     H->far_mode = o->far_mode;
     H->max_chunk = o->max_rhs_chunk;
+    H->precision = o->precision;
   }
   auto cp = [&](std::vector<int32_t>& v, const int32_t* p, int64_t k) { v.assign(p, p + k); };
   cp(H->parent, d->parent, nn);
@@ -714,6 +861,8 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
       H->groups.push_back(std::move(g));
     }
     L.ntiles = int(H->tiles.size()) - L.first_tile;
+    L.first_group = int(H->groups.size()) - int(gs.size());
+    L.ngroups = int(gs.size());
     if (L.ntiles > 0) H->launches.push_back(L);
   };
 
@@ -920,6 +1069,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     H->n_unpack = int32_t(segs.size()) - H->n_pack;
     H->d_segs.upload(segs);
   }
+  if (H->precision == GOFMM_PRECISION_F32) build_f32(H);
 }
 
 void ensure_workspace(gofmm_handle* H, int32_t r) {
@@ -1125,6 +1275,116 @@ void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double*
   }
 }
 
+// ---------------------------------------------------------------- FP32 evaluation
+void ensure_workspace32(gofmm_handle* H, int32_t r) {
+  if (r <= H->ws32_r) return;
+  for (int p = 0; p < 2; ++p) {
+    H->d_wp32[p].alloc(size_t(H->ld_wp) * r * sizeof(float));
+    H->d_what32[p].alloc(size_t(H->ld_s) * r * sizeof(float));
+    H->d_c32[p].alloc(size_t(H->ld_s) * r * sizeof(float));
+  }
+  H->ws32_r = r;
+  H->maps32_r = 0;
+}
+
+// B operand view of an FP32 panel buffer: {16 rows-in-panel, r columns, rows/16 panels}, boxes
+// of 16 x bn, 64-byte swizzle = the K-major SWIZZLE_64B UMMA operand layout
+void encode_bmap32(CUtensorMap* map, const float* ptr, int64_t rows, int32_t r, int32_t r_ws, int bn) {
+  cuuint64_t dims[3] = {16, cuuint64_t(r), cuuint64_t(rows / 16)};
+  cuuint64_t strides[2] = {16 * sizeof(float), cuuint64_t(r_ws) * 16 * sizeof(float)};
+  cuuint32_t box[3] = {16, cuuint32_t(bn), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult rc = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides,
+                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) throw Error(GOFMM_ERR_CUDA, "cuTensorMapEncodeTiled (fp32) failed: " + std::to_string(int(rc)));
+}
+
+void enqueue_chunk32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, float* d_u, int64_t ldu,
+                     cudaStream_t st, bool timed) {
+  ensure_workspace32(H, r);
+  const int bn = f32_bn(r);
+  if (H->k32_s.bn != bn) {
+    H->k32_s = f32::pick_gemm(kKindNone, 1, bn);
+    if (H->kfn_g) H->k32_g = f32::pick_gemm(H->kernel, H->dim, bn);
+    GOFMM_CUDA(cudaGetLastError());
+    H->maps32_r = 0;
+  }
+  if (H->maps32_r != r) {
+    const float* bufs[3][2] = {{H->d_wp32[0].as<float>(), H->d_wp32[1].as<float>()},
+                               {H->d_what32[0].as<float>(), H->d_what32[1].as<float>()},
+                               {H->d_c32[0].as<float>(), H->d_c32[1].as<float>()}};
+    const int64_t rows[3] = {H->ld_wp, H->ld_s, H->ld_s};
+    for (int b = 0; b < 3; ++b)
+      for (int p = 0; p < 2; ++p) encode_bmap32(&H->maps32.m[b][p], bufs[b][p], rows[b], r, H->ws32_r, bn);
+    H->maps32_r = r;
+  }
+  const int64_t pstride = int64_t(H->ws32_r) * 16;
+  if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[0], st));
+  GOFMM_CUDA(f32::launch_permute_in(d_w, ldw, H->d_prow.as<int32_t>(), 0, H->ld_wp, r, H->n, H->d_wp32[0].as<float>(),
+                                    H->d_wp32[1].as<float>(), pstride, st));
+  if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[1], st));
+  int marked = 1;
+  for (const Launch& L : H->launches) {
+    while (timed && marked <= L.phase) GOFMM_CUDA(cudaEventRecord(H->ev[1 + marked++], st));
+    float *ch, *cl;
+    int64_t ldc;
+    int32_t cpanel = 1;
+    switch (L.out) {
+      case Buf::What: ch = H->d_what32[0].as<float>(); cl = H->d_what32[1].as<float>(); ldc = pstride; break;
+      case Buf::C: ch = H->d_c32[0].as<float>(); cl = H->d_c32[1].as<float>(); ldc = pstride; break;
+      default: ch = d_u; cl = nullptr; ldc = ldu; cpanel = 0; break;
+    }
+    const size_t li = size_t(&L - H->launches.data());
+    if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li], st));
+    const f32::GemmKernel& k = L.gen ? H->k32_g : H->k32_s;
+    GOFMM_CUDA(f32::launch_gemm(k, unsigned(L.ntiles32), r, H->maps32, H->d_tiles32.as<Tile>() + L.first_tile32,
+                                H->d_groups.as<Group>(), H->d_terms32.as<f32::Term>(), H->kp32, ch, cl, ldc, cpanel,
+                                st));
+    if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li + 1], st));
+  }
+  if (timed) {
+    while (marked <= 2) GOFMM_CUDA(cudaEventRecord(H->ev[1 + marked++], st));
+    GOFMM_CUDA(cudaEventRecord(H->ev[4], st));
+  }
+  GOFMM_CUDA(cudaGetLastError());
+}
+
+int32_t rhs_chunk32(gofmm_handle* H, int32_t r) {
+  if (H->max_chunk > 0) return std::min(r, H->max_chunk);
+  if (r <= H->ws32_r) return r;
+  size_t free_b = 0, total_b = 0;
+  GOFMM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const double per_col = 8.0 * double(H->ld_wp + 2 * H->ld_s);  // hi + lo floats
+  const double avail = 0.85 * double(free_b) + per_col * H->ws32_r;
+  int64_t cols = int64_t(avail / per_col);
+  if (cols >= r) return r;
+  if (cols >= 256) cols = (cols / 256) * 256;
+  if (cols < 1) throw Error(GOFMM_ERR_CUDA, "not enough device memory for one right-hand side");
+  return int32_t(cols);
+}
+
+void enqueue32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, float* d_u, int64_t ldu, cudaStream_t st,
+               bool timed) {
+  const int32_t rc = rhs_chunk32(H, r);
+  if (timed) {
+    H->launch_ms.assign(H->launches.size(), 0.f);
+    std::fill(std::begin(H->phase_ms), std::end(H->phase_ms), 0.f);
+  }
+  for (int32_t c0 = 0; c0 < r; c0 += rc) {
+    const int32_t rr = std::min(rc, r - c0);
+    enqueue_chunk32(H, d_w + size_t(c0) * ldw, ldw, rr, d_u + size_t(c0) * ldu, ldu, st, timed);
+    if (timed) accumulate_chunk_times(H);
+  }
+}
+
+void check_precision(const gofmm_handle* H, int32_t want) {
+  if (H && H->precision != want)
+    throw Error(GOFMM_ERR_INVALID, want == GOFMM_PRECISION_F32
+                                       ? "fp32 entry point on an fp64 handle (create with precision GOFMM_PRECISION_F32)"
+                                       : "fp64 entry point on an fp32 handle (use the *_f32 entry points)");
+}
+
 void fill_phase_times(gofmm_handle* H, gofmm_eval_stats* s) {
   s->ms_permute = H->phase_ms[0];
   s->ms_upward = H->phase_ms[1];
@@ -1148,7 +1408,7 @@ using namespace gofmm;
 
 extern "C" {
 
-int32_t gofmm_abi_version(void) { return 1; }
+int32_t gofmm_abi_version(void) { return 2; }
 
 const char* gofmm_last_error(void) { return g_last_error.c_str(); }
 
@@ -1266,6 +1526,7 @@ int gofmm_dist_plan_host(const gofmm_tree_desc* d, int32_t rank, int32_t nranks,
 int gofmm_dist_stage1(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double* d_send, void* stream) {
   return guarded([&] {
     check_args(H, d_w, ldw, r, d_w, H->n);
+    check_precision(H, GOFMM_PRECISION_F64);
     if (H->nranks > 1 && !d_send && H->dist.max_send_rows > 0) throw Error(GOFMM_ERR_INVALID, "null send buffer");
     GOFMM_CUDA(cudaSetDevice(H->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
@@ -1276,6 +1537,7 @@ int gofmm_dist_stage1(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r
 int gofmm_dist_stage2(gofmm_handle* H, const double* d_recv, int32_t r, double* d_u, int64_t ldu, void* stream) {
   return guarded([&] {
     check_args(H, d_u, H->n, r, d_u, ldu);
+    check_precision(H, GOFMM_PRECISION_F64);
     if (H->nranks > 1 && !d_recv && H->dist.max_send_rows > 0) throw Error(GOFMM_ERR_INVALID, "null receive buffer");
     if (r > H->ws_r) throw Error(GOFMM_ERR_INVALID, "stage2: r differs from stage1");
     GOFMM_CUDA(cudaSetDevice(H->device));
@@ -1315,7 +1577,10 @@ int gofmm_launch_profile(const gofmm_handle* H, int32_t r, int32_t cap, gofmm_la
       const Launch& L = H->launches[i];
       out[i].phase = L.phase;
       out[i].level = L.level;
-      out[i].ctas = int64_t(L.ntiles) * ((r + (L.gen ? kBN_G : kBN_S) - 1) / (L.gen ? kBN_G : kBN_S));
+      if (H->precision == GOFMM_PRECISION_F32)
+        out[i].ctas = int64_t(L.ntiles32) * ((r + f32_bn(r) - 1) / f32_bn(r));
+      else
+        out[i].ctas = int64_t(L.ntiles) * ((r + (L.gen ? kBN_G : kBN_S) - 1) / (L.gen ? kBN_G : kBN_S));
       out[i].flops = L.flops_per_rhs * int64_t(r);
       out[i].ms = i < int32_t(H->launch_ms.size()) ? H->launch_ms[i] : -1.0;
       out[i].generated = L.gen ? 1 : 0;
@@ -1329,7 +1594,9 @@ int64_t gofmm_device_bytes(const gofmm_handle* H) {
   if (!H) return -1;
   const DevBuf* bufs[] = {&H->d_proj, &H->d_diag, &H->d_near,  &H->d_far,   &H->d_xp,   &H->d_xs,
                           &H->d_prow, &H->d_iperm, &H->d_tiles, &H->d_groups, &H->d_terms, &H->d_wp,
-                          &H->d_what, &H->d_c,    &H->d_win,   &H->d_uout};
+                          &H->d_what, &H->d_c,    &H->d_win,   &H->d_uout, &H->d_a32h, &H->d_a32l,
+                          &H->d_xp32, &H->d_xs32, &H->d_terms32, &H->d_tiles32, &H->d_wp32[0], &H->d_wp32[1],
+                          &H->d_what32[0], &H->d_what32[1], &H->d_c32[0], &H->d_c32[1], &H->d_win32, &H->d_uout32};
   int64_t s = 0;
   for (auto* b : bufs) s += int64_t(b->bytes);
   return s;
@@ -1339,6 +1606,7 @@ int gofmm_evaluate_device(gofmm_handle* H, const double* d_w, int64_t ldw, int32
                           void* stream, int32_t stats_sync, gofmm_eval_stats* stats) {
   return guarded([&] {
     check_args(H, d_w, ldw, r, d_u, ldu);
+    check_precision(H, GOFMM_PRECISION_F64);
     GOFMM_CUDA(cudaSetDevice(H->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
     auto t0 = std::chrono::steady_clock::now();
@@ -1354,61 +1622,117 @@ int gofmm_evaluate_device(gofmm_handle* H, const double* d_w, int64_t ldw, int32
   });
 }
 
+}  // extern "C"
+
+namespace {
+// Host-buffer evaluation (the drop-in for gfmm::evaluate): W column chunks are staged into HBM,
+// evaluated, and u_perm copied back; h2d / d2h are timed with events on the handle's stream.
+template <class T>
+void evaluate_host(gofmm_handle* H, const T* w, int64_t ldw, int32_t r, T* u_perm, int64_t ldu,
+                   gofmm_eval_stats* stats) {
+  constexpr bool kF32 = sizeof(T) == 4;
+  check_args(H, w, ldw, r, u_perm, ldu);
+  check_precision(H, kF32 ? GOFMM_PRECISION_F32 : GOFMM_PRECISION_F64);
+  GOFMM_CUDA(cudaSetDevice(H->device));
+  auto t0 = std::chrono::steady_clock::now();
+  cudaStream_t st = H->stream;
+  DevBuf& win = kF32 ? H->d_win32 : H->d_win;
+  DevBuf& uout = kF32 ? H->d_uout32 : H->d_uout;
+  // device staging for W and u (a column chunk at a time when r does not fit)
+  const int32_t rc_ws = kF32 ? rhs_chunk32(H, r) : rhs_chunk(H, r);
+  size_t free_b = 0, total_b = 0;
+  GOFMM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const size_t per_col = size_t(H->n) * sizeof(T);
+  int32_t rc = std::min<int32_t>(
+      r, std::max<int32_t>(1, int32_t(std::min<size_t>(size_t(rc_ws), (free_b / 2 + win.bytes) / (2 * per_col)))));
+  const size_t bytes = per_col * size_t(rc);
+  if (win.bytes < bytes) {
+    win.alloc(bytes, false);
+    uout.alloc(bytes, false);
+  }
+  float h2d = 0, d2h = 0, ph[4] = {0, 0, 0, 0};
+  std::vector<float> lms(H->launches.size(), 0.f);
+  for (int32_t c0 = 0; c0 < r; c0 += rc) {
+    const int32_t rr = std::min(rc, r - c0);
+    GOFMM_CUDA(cudaEventRecord(H->ev[5], st));
+    GOFMM_CUDA(cudaMemcpy2DAsync(win.p, per_col, w + size_t(c0) * ldw, size_t(ldw) * sizeof(T), per_col, rr,
+                                 cudaMemcpyHostToDevice, st));
+    GOFMM_CUDA(cudaEventRecord(H->ev[6], st));
+    if constexpr (kF32)
+      enqueue32(H, win.as<float>(), H->n, rr, uout.as<float>(), H->n, st, stats != nullptr);
+    else
+      enqueue(H, win.as<double>(), H->n, rr, uout.as<double>(), H->n, st, stats != nullptr);
+    GOFMM_CUDA(cudaEventRecord(H->ev[4], st));
+    GOFMM_CUDA(cudaMemcpy2DAsync(u_perm + size_t(c0) * ldu, size_t(ldu) * sizeof(T), uout.p, per_col, per_col, rr,
+                                 cudaMemcpyDeviceToHost, st));
+    GOFMM_CUDA(cudaEventRecord(H->ev[7], st));
+    GOFMM_CUDA(cudaStreamSynchronize(st));
+    if (stats) {
+      float a, b;
+      GOFMM_CUDA(cudaEventElapsedTime(&a, H->ev[5], H->ev[6]));
+      GOFMM_CUDA(cudaEventElapsedTime(&b, H->ev[4], H->ev[7]));
+      h2d += a;
+      d2h += b;
+      for (int i = 0; i < 4; ++i) ph[i] += H->phase_ms[i];
+      for (size_t i = 0; i < lms.size(); ++i) lms[i] += H->launch_ms[i];
+    }
+  }
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->flops = H->flops_per_rhs * int64_t(r);
+    std::copy(ph, ph + 4, H->phase_ms);
+    H->launch_ms = lms;
+    fill_phase_times(H, stats);
+    stats->ms_h2d = h2d;
+    stats->ms_d2h = d2h;
+    stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+}
+}  // namespace
+
+extern "C" {
+
 int gofmm_evaluate(gofmm_handle* H, const double* w, int64_t ldw, int32_t r, double* u_perm, int64_t ldu,
                    gofmm_eval_stats* stats) {
+  return guarded([&] { evaluate_host<double>(H, w, ldw, r, u_perm, ldu, stats); });
+}
+
+int gofmm_evaluate_f32(gofmm_handle* H, const float* w, int64_t ldw, int32_t r, float* u_perm, int64_t ldu,
+                       gofmm_eval_stats* stats) {
+  return guarded([&] { evaluate_host<float>(H, w, ldw, r, u_perm, ldu, stats); });
+}
+
+int gofmm_evaluate_device_f32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, float* d_u, int64_t ldu,
+                              void* stream, int32_t stats_sync, gofmm_eval_stats* stats) {
   return guarded([&] {
-    check_args(H, w, ldw, r, u_perm, ldu);
+    check_args(H, d_w, ldw, r, d_u, ldu);
+    check_precision(H, GOFMM_PRECISION_F32);
     GOFMM_CUDA(cudaSetDevice(H->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
     auto t0 = std::chrono::steady_clock::now();
-    cudaStream_t st = H->stream;
-    // device staging for W and u (a column chunk at a time when r does not fit)
-    const int32_t rc_ws = rhs_chunk(H, r);
-    size_t free_b = 0, total_b = 0;
-    GOFMM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const size_t per_col = size_t(H->n) * sizeof(double);
-    int32_t rc = std::min<int32_t>(r, std::max<int32_t>(1, int32_t(std::min<size_t>(
-                                          size_t(rc_ws), (free_b / 2 + H->d_win.bytes) / (2 * per_col)))));
-    const size_t bytes = per_col * size_t(rc);
-    if (H->d_win.bytes < bytes) {
-      H->d_win.alloc(bytes, false);
-      H->d_uout.alloc(bytes, false);
-    }
-    float h2d = 0, d2h = 0, ph[4] = {0, 0, 0, 0};
-    std::vector<float> lms(H->launches.size(), 0.f);
-    for (int32_t c0 = 0; c0 < r; c0 += rc) {
-      const int32_t rr = std::min(rc, r - c0);
-      GOFMM_CUDA(cudaEventRecord(H->ev[5], st));
-      GOFMM_CUDA(cudaMemcpy2DAsync(H->d_win.p, per_col, w + size_t(c0) * ldw, size_t(ldw) * sizeof(double), per_col,
-                                   rr, cudaMemcpyHostToDevice, st));
-      GOFMM_CUDA(cudaEventRecord(H->ev[6], st));
-      enqueue(H, H->d_win.as<double>(), H->n, rr, H->d_uout.as<double>(), H->n, st, stats != nullptr);
-      GOFMM_CUDA(cudaEventRecord(H->ev[4], st));
-      GOFMM_CUDA(cudaMemcpy2DAsync(u_perm + size_t(c0) * ldu, size_t(ldu) * sizeof(double), H->d_uout.p, per_col,
-                                   per_col, rr, cudaMemcpyDeviceToHost, st));
-      GOFMM_CUDA(cudaEventRecord(H->ev[7], st));
-      GOFMM_CUDA(cudaStreamSynchronize(st));
-      if (stats) {
-        float a, b;
-        GOFMM_CUDA(cudaEventElapsedTime(&a, H->ev[5], H->ev[6]));
-        GOFMM_CUDA(cudaEventElapsedTime(&b, H->ev[4], H->ev[7]));
-        h2d += a;
-        d2h += b;
-        for (int i = 0; i < 4; ++i) ph[i] += H->phase_ms[i];
-        for (size_t i = 0; i < lms.size(); ++i) lms[i] += H->launch_ms[i];
-      }
-    }
+    enqueue32(H, d_w, ldw, r, d_u, ldu, st, stats && stats_sync);
     if (stats) {
       std::memset(stats, 0, sizeof(*stats));
       stats->flops = H->flops_per_rhs * int64_t(r);
-      std::copy(ph, ph + 4, H->phase_ms);
-      H->launch_ms = lms;
-      fill_phase_times(H, stats);
-      stats->ms_h2d = h2d;
-      stats->ms_d2h = d2h;
-      stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (stats_sync) {
+        fill_phase_times(H, stats);
+        stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      }
     }
   });
 }
+
+int gofmm_unpermute_device_f32(gofmm_handle* H, const float* d_up, int64_t ldp, int32_t r, float* d_u, int64_t ldu,
+                               void* stream) {
+  return guarded([&] {
+    check_args(H, d_up, ldp, r, d_u, ldu);
+    GOFMM_CUDA(cudaSetDevice(H->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    GOFMM_CUDA(f32::launch_unpermute(d_up, ldp, H->d_iperm.as<int32_t>(), H->n, r, d_u, ldu, st));
+  });
+}
+
+int32_t gofmm_precision(const gofmm_handle* H) { return H ? H->precision : -1; }
 
 // Exact rows of K W for error_eps2 (evaluate.hpp:353: oracle.block(rows, all) * w), matrix-free:
 // one generated term per leaf (K(x_rows, x_leaf) W_perm[leaf]) split over kExactChunks partial
@@ -1555,6 +1879,7 @@ int gofmm_unpermute_device(gofmm_handle* H, const double* d_up, int64_t ldp, int
                            void* stream) {
   return guarded([&] {
     check_args(H, d_up, ldp, r, d_u, ldu);
+    check_precision(H, GOFMM_PRECISION_F64);
     GOFMM_CUDA(cudaSetDevice(H->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
     const int cpb = 8;

@@ -1,0 +1,151 @@
+// gofmm_f32.cu — FP32 (3xTF32 tcgen05) kernel instantiations and launch wrappers.
+// A separate translation unit from the C-ABI (gofmm_capi.cu) so the two compile in parallel;
+// the C-ABI reaches everything here through the entry points declared in gofmm_kernels_f32.cuh.
+#include "gofmm_kernels_f32.cuh"
+
+#include <algorithm>
+
+namespace gofmm {
+namespace f32 {
+namespace {
+
+// ------------------------------------------------------------------ data movement (FP32 path)
+// wp_{hi,lo}[t, c] = split(w[prow[t], c]) in 16-row panels (evaluate.hpp:294-295)
+static __global__ void permute_rows_in_f32(const float* __restrict__ w, int64_t ldw, const int32_t* __restrict__ prow,
+                                    int64_t row0, int64_t row1, int32_t r, int32_t cols_per_block,
+                                    float* __restrict__ wh, float* __restrict__ wl, int64_t pstride) {
+  const int64_t t = row0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= row1) return;
+  const int32_t src = prow[t];
+  const int c0 = blockIdx.y * cols_per_block;
+  const int c1 = min(r, c0 + cols_per_block);
+  const int64_t o = (t >> 4) * pstride + (t & 15);
+  for (int c = c0; c < c1; ++c) {
+    const float x = (src >= 0) ? __ldg(w + src + size_t(c) * ldw) : 0.f;
+    float hi, lo;
+    split_tf32(x, hi, lo);
+    wh[o + size_t(c) * 16] = hi;
+    wl[o + size_t(c) * 16] = lo;
+  }
+}
+
+// u[iperm[t], c] = up[t, c]
+static __global__ void unpermute_rows_f32(const float* __restrict__ up, int64_t ldp, const int32_t* __restrict__ iperm,
+                                   int64_t n, int32_t r, int32_t cols_per_block, float* __restrict__ u, int64_t ldu) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int32_t dst = iperm[t];
+  const int c0 = blockIdx.y * cols_per_block;
+  const int c1 = min(r, c0 + cols_per_block);
+  for (int c = c0; c < c1; ++c) u[dst + size_t(c) * ldu] = up[t + size_t(c) * ldp];
+}
+
+static __global__ void split_to_kmajor(const SplitJob* __restrict__ jobs, float* __restrict__ hi, float* __restrict__ lo) {
+  const SplitJob J = jobs[blockIdx.x];
+  const int64_t n = int64_t(J.rows) * J.ldd;
+  for (int64_t e = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.y) * blockDim.x) {
+    const int m = int(e / J.ldd), k = int(e % J.ldd);
+    double x = 0.0;
+    if (k < J.cols) x = J.trans ? J.src[m + size_t(k) * J.lds] : J.src[k + size_t(m) * J.lds];
+    float h, l;
+    split_tf32(float(x), h, l);
+    hi[J.dst + e] = h;
+    lo[J.dst + e] = float(x - double(h));  // the FP64 residual: hi + lo carries ~2^-35 more
+  }
+}
+
+static __global__ void to_f32(const double* __restrict__ x, int64_t n, float* __restrict__ y) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    y[i] = float(x[i]);
+}
+
+
+template <int BN>
+constexpr int stages_for() {
+  return BN == 256 ? 4 : BN == 128 ? 6 : 8;  // ~192 KB of pipeline in every configuration
+}
+
+template <int KIND, int DIM, int BN>
+GemmKernel make_kernel() {
+  constexpr int ST = stages_for<BN>();
+  GemmKernel k;
+  k.fn = &grouped_gemm_tf32x3<BN, ST, KIND, DIM>;
+  k.smem = Shape<BN, ST>::smem_bytes;
+  k.bn = BN;
+  return k;
+}
+
+template <int KIND, int DIM>
+GemmKernel by_bn(int bn) {
+  if (bn <= 64) return make_kernel<KIND, DIM, 64>();
+  if (bn <= 128) return make_kernel<KIND, DIM, 128>();
+  return make_kernel<KIND, DIM, 256>();
+}
+
+template <int KIND>
+GemmKernel by_dim(int dim, int bn) {
+  switch (dim) {
+    case 3: return by_bn<KIND, 3>(bn);
+    case 8: return by_bn<KIND, 8>(bn);
+    default: return by_bn<KIND, 0>(bn);
+  }
+}
+
+}  // namespace
+
+GemmKernel pick_gemm(int kind, int dim, int bn) {
+  GemmKernel k;
+  switch (kind) {
+    case kKindNone: k = by_bn<kKindNone, 1>(bn); break;
+    case kGaussian: k = by_dim<kGaussian>(dim, bn); break;
+    case kLaplace: k = by_dim<kLaplace>(dim, bn); break;
+    case kPolynomial: k = by_dim<kPolynomial>(dim, bn); break;
+    case kExponential: k = by_dim<kExponential>(dim, bn); break;
+    default: return k;
+  }
+  cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(k.smem));
+  return k;
+}
+
+cudaError_t launch_gemm(const GemmKernel& k, unsigned ntiles, int32_t R, const BMaps& maps, const Tile* tiles,
+                        const Group* groups, const Term* terms, const KernelParams& kp, float* c_hi, float* c_lo,
+                        int64_t ldc, int32_t cpanel, cudaStream_t st) {
+  dim3 grid(ntiles, unsigned((R + k.bn - 1) / k.bn));
+  k.fn<<<grid, kThreads, k.smem, st>>>(maps, tiles, groups, terms, R, kp, c_hi, c_lo, ldc, cpanel);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_permute_in(const float* w, int64_t ldw, const int32_t* prow, int64_t row0, int64_t row1, int32_t r,
+                              int64_t n, float* wh, float* wl, int64_t pstride, cudaStream_t st) {
+  if (row1 <= row0) return cudaSuccess;
+  // blocks walk all rows of cpb columns before the next ones: the randomly gathered source
+  // columns stay L2-resident (see the FP64 permutation in gofmm_capi.cu)
+  const int cpb = int(std::max<int64_t>(1, std::min<int64_t>(8, (48ll << 20) / (std::max<int64_t>(n, 1) * 4))));
+  dim3 grid(unsigned((row1 - row0 + 255) / 256), unsigned((r + cpb - 1) / cpb));
+  permute_rows_in_f32<<<grid, 256, 0, st>>>(w, ldw, prow, row0, row1, r, cpb, wh, wl, pstride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpermute(const float* up, int64_t ldp, const int32_t* iperm, int64_t n, int32_t r, float* u,
+                             int64_t ldu, cudaStream_t st) {
+  const int cpb = 8;
+  dim3 grid(unsigned((n + 255) / 256), unsigned((r + cpb - 1) / cpb));
+  unpermute_rows_f32<<<grid, 256, 0, st>>>(up, ldp, iperm, n, r, cpb, u, ldu);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_split(const SplitJob* d_jobs, int njobs, float* hi, float* lo, cudaStream_t st) {
+  if (njobs <= 0) return cudaSuccess;
+  dim3 grid(unsigned(njobs), 16);
+  split_to_kmajor<<<grid, 256, 0, st>>>(d_jobs, hi, lo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_to_f32(const double* x, int64_t n, float* y, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  to_f32<<<unsigned(std::min<int64_t>((n + 255) / 256, 4096)), 256, 0, st>>>(x, n, y);
+  return cudaGetLastError();
+}
+
+}  // namespace f32
+}  // namespace gofmm

@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
 // wp[t, c] = w[prow[t], c]   (evaluate.hpp:294-295) into the padded leaf layout, stored in
 // 16-row panels (panel stride `pstride` doubles); prow = -1 marks padding rows (written as 0).
 // Rows [row0, row1) only (a rank's own leaves in a distributed evaluation).
-__global__ void permute_rows_in(const double* __restrict__ w, int64_t ldw, const int32_t* __restrict__ prow,
+static __global__ void permute_rows_in(const double* __restrict__ w, int64_t ldw, const int32_t* __restrict__ prow,
                                 int64_t row0, int64_t row1, int32_t r, int32_t cols_per_block,
                                 double* __restrict__ wp, int64_t pstride) {
   const int64_t t = row0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -604,7 +604,7 @@ struct PanelSeg {
   int64_t rows;     // multiple of 16
 };
 
-__global__ void panel_copy(const PanelSeg* __restrict__ segs, double* __restrict__ what, double* __restrict__ wp,
+static __global__ void panel_copy(const PanelSeg* __restrict__ segs, double* __restrict__ what, double* __restrict__ wp,
                            int64_t ws_pstride, double* __restrict__ buf, int32_t r, int32_t to_buffer) {
   const PanelSeg sg = segs[blockIdx.x];
   double* ws = (sg.buf == 0) ? what : wp;
@@ -621,7 +621,7 @@ __global__ void panel_copy(const PanelSeg* __restrict__ segs, double* __restrict
 }
 
 // out[i, c] = sum_p part[p*nrows + i, c]  (fixed order over the partials: deterministic)
-__global__ void sum_partials(const double* __restrict__ part, int64_t ldp, int32_t nrows, int32_t nparts, int32_t r,
+static __global__ void sum_partials(const double* __restrict__ part, int64_t ldp, int32_t nrows, int32_t nparts, int32_t r,
                              double* __restrict__ out, int64_t ldo) {
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= int64_t(nrows) * r) return;
@@ -632,7 +632,7 @@ __global__ void sum_partials(const double* __restrict__ part, int64_t ldp, int32
 }
 
 // u[iperm[t], c] = up[t, c]   (unpermute, evaluate.hpp:21-25)
-__global__ void unpermute_rows(const double* __restrict__ up, int64_t ldp, const int32_t* __restrict__ iperm,
+static __global__ void unpermute_rows(const double* __restrict__ up, int64_t ldp, const int32_t* __restrict__ iperm,
                                int64_t n, int32_t r, int32_t cols_per_block, double* __restrict__ u, int64_t ldu) {
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= n) return;

@@ -154,12 +154,19 @@ class Evaluator:
 
     def __init__(self, tree: CompressedTree, device: int = 0, near_mode: int = L.BLOCKS_MATRIX_FREE,
                  far_mode: int = L.BLOCKS_MATRIX_FREE, stored: bool | None = None, max_rhs_chunk: int = 0,
-                 rank: int | None = None, nranks: int = 1):
+                 rank: int | None = None, nranks: int = 1, precision: str = "fp64"):
+        """precision "fp64" (the reference's arithmetic, common.hpp:18) or "fp32" (north_star's
+        1e-5 class: 3xTF32 on the tcgen05 tensor cores; W / u are float32)."""
+        if precision not in ("fp64", "fp32"):
+            raise L.InvalidArgument(L.GOFMM_ERR_INVALID, f"precision must be 'fp64' or 'fp32', not {precision!r}")
         self.tree = tree
         self.n = int(tree.n)
+        self.precision = precision
+        self.dtype = np.float64 if precision == "fp64" else np.float32
         lib = L.lib()
         d, keep, use_stored = make_desc(tree, stored)
-        o = L.Options(device, near_mode, far_mode, max_rhs_chunk)
+        o = L.Options(device, near_mode, far_mode, max_rhs_chunk,
+                      L.PRECISION_F64 if precision == "fp64" else L.PRECISION_F32)
         h = C.c_void_p()
         if rank is None:
             L.check(lib.gofmm_create(C.byref(d), C.byref(o), C.byref(h)))
@@ -218,7 +225,7 @@ class Evaluator:
     def evaluate(self, w: np.ndarray, out: np.ndarray | None = None) -> Potentials:
         """u_perm = K~ w from HOST memory (the drop-in for gfmm::evaluate; evaluate.hpp:287-317).
         `out` (optional, N x r Fortran-ordered, e.g. a pinned buffer) receives u_perm."""
-        w = np.asarray(w, dtype=np.float64)
+        w = np.asarray(w, dtype=self.dtype)
         if w.ndim == 1:
             w = w.reshape(-1, 1)
         if w.shape[0] != self.n:
@@ -228,14 +235,16 @@ class Evaluator:
         w = np.asfortranarray(w)
         r = int(w.shape[1])
         if out is None:
-            u = np.empty((self.n, r), dtype=np.float64, order="F")
+            u = np.empty((self.n, r), dtype=self.dtype, order="F")
         else:
             u = out
-            if u.shape != (self.n, r) or u.dtype != np.float64 or not u.flags.f_contiguous:
-                raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "evaluate: out must be N x r float64 Fortran order")
+            if u.shape != (self.n, r) or u.dtype != self.dtype or not u.flags.f_contiguous:
+                raise L.InvalidArgument(L.GOFMM_ERR_INVALID,
+                                        f"evaluate: out must be N x r {np.dtype(self.dtype).name} Fortran order")
         st = L.EvalStats()
         t0 = time.perf_counter()
-        L.check(L.lib().gofmm_evaluate(self._h, _p(w), self.n, r, _p(u), self.n, C.byref(st)))
+        fn = L.lib().gofmm_evaluate if self.precision == "fp64" else L.lib().gofmm_evaluate_f32
+        L.check(fn(self._h, _p(w), self.n, r, _p(u), self.n, C.byref(st)))
         secs = time.perf_counter() - t0
         return Potentials(u=u, flops=int(st.flops), seconds=secs, stats=_stats(st))
 
@@ -243,9 +252,10 @@ class Evaluator:
                         sync_stats: bool = False) -> dict:
         """Device-pointer variant (W and u_perm already resident in HBM); enqueues on `stream`."""
         st = L.EvalStats()
+        fn = L.lib().gofmm_evaluate_device if self.precision == "fp64" else L.lib().gofmm_evaluate_device_f32
         # torch's default stream is the legacy NULL stream: pass cudaStreamLegacy (0x1) explicitly,
         # because NULL selects the handle's own stream in the C-ABI
-        L.check(L.lib().gofmm_evaluate_device(self._h, C.c_void_p(w_ptr), ldw, r, C.c_void_p(u_ptr), ldu,
+        L.check(fn(self._h, C.c_void_p(w_ptr), ldw, r, C.c_void_p(u_ptr), ldu,
                                               C.c_void_p(stream if stream else 1), 1 if sync_stats else 0,
                                               C.byref(st)))
         return _stats(st)
@@ -254,12 +264,13 @@ class Evaluator:
         """u_perm = K~ w for CUDA torch tensors (column-major = transposed contiguous views)."""
         import torch
 
-        if not (w.is_cuda and w.dtype == torch.float64):
-            raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "evaluate_torch: w must be a CUDA float64 tensor")
+        tdt = torch.float64 if self.precision == "fp64" else torch.float32
+        if not (w.is_cuda and w.dtype == tdt):
+            raise L.InvalidArgument(L.GOFMM_ERR_INVALID, f"evaluate_torch: w must be a CUDA {tdt} tensor")
         wt = _colmajor(w)
         r = int(w.shape[1])
         if out is None:
-            out = torch.empty((r, self.n), dtype=torch.float64, device=w.device).t()
+            out = torch.empty((r, self.n), dtype=tdt, device=w.device).t()
         stream = torch.cuda.current_stream(w.device).cuda_stream
         stats = self.evaluate_device(wt.data_ptr(), wt.stride(1), r, out.data_ptr(), out.stride(1), stream,
                                      sync_stats)

@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(L.EXPORTS)
-    assert lib.gofmm_abi_version() == 1
+    assert lib.gofmm_abi_version() == 2  # 2: gofmm_options.precision + the *_f32 entry points
 
 
 def _desc_from_tree(t, keep):
