@@ -377,7 +377,7 @@ struct gofmm_handle {
   // hi / lo copies (d_a32h / d_a32l, offsets per term), FP32 coordinates, 128-row tiles, and a
   // workspace of hi / lo panel buffers [0] = hi, [1] = lo
   int32_t precision = GOFMM_PRECISION_F64;
-  gofmm::DevBuf d_a32h, d_a32l, d_xp32, d_xs32, d_terms32, d_tiles32;
+  gofmm::DevBuf d_a32h, d_a32l, d_xp32, d_xs32, d_xpn32, d_xsn32, d_terms32, d_tiles32;
   std::vector<int64_t> term_a32_off, term_a32_ld;  // per plan term (flattened group order), -1 if generated
   gofmm::DevBuf d_wp32[2], d_what32[2], d_c32[2], d_win32, d_uout32;
   int32_t ws32_r = 0;
@@ -493,6 +493,15 @@ void build_f32(gofmm_handle* H) {
     H->d_xs32.alloc(size_t(std::max<int64_t>(nxs, 1)) * sizeof(float), false);
     GOFMM_CUDA(f32::launch_to_f32(H->d_xp.as<double>(), nxp, H->d_xp32.as<float>(), H->stream));
     if (H->d_xs.p) GOFMM_CUDA(f32::launch_to_f32(H->d_xs.as<double>(), nxs, H->d_xs32.as<float>(), H->stream));
+    if (H->kernel == kGaussian) {
+      // norm expansion operands: -log2(e)/(2h^2) |x|^2, from the FP64 coordinates
+      const double sc = -H->kp.p0 * 1.4426950408889634;
+      H->d_xpn32.alloc(size_t(std::max<int64_t>(H->ld_wp, 16)) * sizeof(float));
+      H->d_xsn32.alloc(size_t(std::max<int64_t>(H->ld_s, 16)) * sizeof(float));
+      GOFMM_CUDA(f32::launch_scaled_norms(H->d_xp.as<double>(), H->ld_wp, H->dim, sc, H->d_xpn32.as<float>(), H->stream));
+      if (H->d_xs.p)
+        GOFMM_CUDA(f32::launch_scaled_norms(H->d_xs.as<double>(), H->ld_s, H->dim, sc, H->d_xsn32.as<float>(), H->stream));
+    }
     GOFMM_CUDA(cudaStreamSynchronize(H->stream));
   }
   // kernel parameters: exp(x) = 2^(x log2 e) is folded into the scale (ex2.approx in the kernel)
@@ -518,6 +527,7 @@ void build_f32(gofmm_handle* H) {
   std::vector<Group> gs;
   std::vector<f32::Term> ts;
   const float* xb[2] = {H->d_xp32.as<float>(), H->d_xs32.as<float>()};
+  const float* xn[2] = {H->d_xpn32.as<float>(), H->d_xsn32.as<float>()};
   const int bid[4] = {kBufWp, kBufWhat, kBufC, kBufC};
   size_t ti = 0;
   for (const HostGroup& hg : H->groups) {
@@ -534,6 +544,10 @@ void build_f32(gofmm_handle* H) {
         t.flags = kTermGen;
         t.xr = xb[ht.x_blob] + ht.xr_off * H->dim;
         t.xc = xb[ht.x_blob] + ht.xc_off * H->dim;
+        if (xn[ht.x_blob]) {
+          t.xrn = xn[ht.x_blob] + ht.xr_off;
+          t.xcn = xn[ht.x_blob] + ht.xc_off;
+        }
       } else {
         t.a_hi = H->d_a32h.as<float>() + H->term_a32_off[ti];
         t.a_lo = H->d_a32l.as<float>() + H->term_a32_off[ti];
@@ -1595,7 +1609,7 @@ int64_t gofmm_device_bytes(const gofmm_handle* H) {
   const DevBuf* bufs[] = {&H->d_proj, &H->d_diag, &H->d_near,  &H->d_far,   &H->d_xp,   &H->d_xs,
                           &H->d_prow, &H->d_iperm, &H->d_tiles, &H->d_groups, &H->d_terms, &H->d_wp,
                           &H->d_what, &H->d_c,    &H->d_win,   &H->d_uout, &H->d_a32h, &H->d_a32l,
-                          &H->d_xp32, &H->d_xs32, &H->d_terms32, &H->d_tiles32, &H->d_wp32[0], &H->d_wp32[1],
+                          &H->d_xp32, &H->d_xs32, &H->d_xpn32, &H->d_xsn32, &H->d_terms32, &H->d_tiles32, &H->d_wp32[0], &H->d_wp32[1],
                           &H->d_what32[0], &H->d_what32[1], &H->d_c32[0], &H->d_c32[1], &H->d_win32, &H->d_uout32};
   int64_t s = 0;
   for (auto* b : bufs) s += int64_t(b->bytes);

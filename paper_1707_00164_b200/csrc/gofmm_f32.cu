@@ -60,6 +60,16 @@ static __global__ void to_f32(const double* __restrict__ x, int64_t n, float* __
 }
 
 
+// out[p] = float(scale * |x_p|^2) in FP64 (Gaussian norm expansion operands)
+static __global__ void scaled_norms(const double* __restrict__ x, int64_t npts, int dim, double scale,
+                                    float* __restrict__ out) {
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < npts; p += int64_t(gridDim.x) * blockDim.x) {
+    double s2 = 0.0;
+    for (int q = 0; q < dim; ++q) s2 = fma(x[p * dim + q], x[p * dim + q], s2);
+    out[p] = float(scale * s2);
+  }
+}
+
 template <int BN>
 constexpr int stages_for() {
   return BN == 256 ? 4 : BN == 128 ? 6 : 8;  // ~192 KB of pipeline in every configuration
@@ -138,6 +148,12 @@ cudaError_t launch_split(const SplitJob* d_jobs, int njobs, float* hi, float* lo
   if (njobs <= 0) return cudaSuccess;
   dim3 grid(unsigned(njobs), 16);
   split_to_kmajor<<<grid, 256, 0, st>>>(d_jobs, hi, lo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scaled_norms(const double* x, int64_t npts, int dim, double scale, float* out, cudaStream_t st) {
+  if (npts <= 0) return cudaSuccess;
+  scaled_norms<<<unsigned(std::min<int64_t>((npts + 255) / 256, 4096)), 256, 0, st>>>(x, npts, dim, scale, out);
   return cudaGetLastError();
 }
 

@@ -38,6 +38,8 @@ struct Term {
   const float* a_lo;
   const float* xr;  // generated: row points (point-major FP32, `dim` floats per point)
   const float* xc;  // generated: column points
+  const float* xrn;  // Gaussian: -log2(e)/(2h^2) |x|^2 of the row / column points (from FP64)
+  const float* xcn;
   int64_t lda;
   int64_t b_row;  // first row of B inside buffer `bbuf` (16-aligned)
   int32_t K;
@@ -84,10 +86,13 @@ template <int BN, int STAGES>
 struct Shape {
   static_assert(BN % 32 == 0 && BN >= 64 && BN <= 256, "UMMA N");
   static constexpr int kBTileBytes = BN * kBK * 4;
-  static constexpr int kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;
+  // column point coordinates of a generated stage (16 x dim floats) + their scaled norms (16)
+  static constexpr int kXBytes = kBK * (kMaxDimRt + 1) * 4 + 64;
+  static constexpr int kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;  // 1024-aligned (swizzle atoms)
   static constexpr int kTmemCols = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;  // ping-pong pair
   static constexpr int kBars = 3 * STAGES + 4;  // full_a, full_b, empty, tmem_full[2], tmem_empty[2]
-  static constexpr size_t smem_bytes = 1024 + size_t(STAGES) * kStageBytes + size_t(kBars) * 8 + 16;
+  static constexpr size_t smem_bytes =
+      1024 + size_t(STAGES) * (kStageBytes + kXBytes) + size_t(kBars) * 8 + 16;
 };
 
 // ------------------------------------------------------------------ tcgen05 / proxy helpers
@@ -157,7 +162,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 template <int KIND>
 __device__ __forceinline__ float entry_from(float d2_or_ip, const KernelParams& kp) {
   if constexpr (KIND == kGaussian) {
-    return ex2_approx(-d2_or_ip * kp.p0);
+    return ex2_approx(d2_or_ip);  // argument already -p0' d^2 (norm expansion in the kernel)
   } else if constexpr (KIND == kExponential) {
     return ex2_approx(-sqrtf(d2_or_ip) * kp.p0);
   } else if constexpr (KIND == kLaplace) {
@@ -202,7 +207,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   // stage s: [A_hi | A_lo | B_hi | B_lo]
   const uint32_t sbase = smem_u32(base);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + STAGES * S::kStageBytes);
+  // [STAGES x (A_hi | A_lo | B_hi | B_lo)] [STAGES x X] [barriers] [TMEM address]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + STAGES * (S::kStageBytes + S::kXBytes));
   // full_a[S] (A producers, 8 warp arrivals), full_b[S] (TMA tx), empty[S] (MMA commit),
   // tmem_full[2] (MMA commit at a segment end), tmem_empty[2] (8 drain-warp arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S::kBars);
@@ -212,6 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto bar_tfull = [&](int b) { return smem_u32(&bars[3 * STAGES + b]); };
   auto bar_tempty = [&](int b) { return smem_u32(&bars[3 * STAGES + 2 + b]); };
   auto a_tile = [&](int s, int part) { return sbase + uint32_t(s * S::kStageBytes + part * kATileBytes); };
+  auto x_tile = [&](int s) { return sbase + uint32_t(STAGES * S::kStageBytes + s * S::kXBytes); };
   auto b_tile = [&](int s, int part) {
     return sbase + uint32_t(s * S::kStageBytes + 2 * kATileBytes + part * S::kBTileBytes);
   };
@@ -274,9 +281,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(bar_empty(st), ((s / STAGES) & 1) ^ 1);
         const Term& T = terms[t];
         const int32_t panel = int32_t((T.b_row + k) >> 4);
-        mbar_arrive_expect_tx(bar_full_b(st), 2 * S::kBTileBytes);
+        // generated stage: the 16 column points' coordinates ride on the same barrier (one bulk
+        // copy of 64*dim contiguous bytes; rows past K are padding points of the same buffer)
+        const bool gen = kGen && (T.flags & kTermGen);
+        const uint32_t xbytes = gen ? uint32_t(kBK * 4 * ((DIM > 0) ? DIM : kp.dim)) : 0u;
+        constexpr uint32_t nbytes = (KIND == kGaussian) ? uint32_t(kBK * 4) : 0u;
+        mbar_arrive_expect_tx(bar_full_b(st), 2 * S::kBTileBytes + xbytes + (gen ? nbytes : 0u));
         tma_load_3d(b_tile(st, 0), &maps.m[T.bbuf][0], 0, n0, panel, bar_full_b(st));
         tma_load_3d(b_tile(st, 1), &maps.m[T.bbuf][1], 0, n0, panel, bar_full_b(st));
+        if (gen)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                  x_tile(st)),
+              "l"(T.xc + size_t(k) * ((DIM > 0) ? DIM : kp.dim)), "r"(xbytes), "r"(bar_full_b(st))
+              : "memory");
+        if (gen && nbytes)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                  x_tile(st) + uint32_t(kBK * (kMaxDimRt + 1) * 4)),
+              "l"(T.xcn + k), "r"(nbytes), "r"(bar_full_b(st))
+              : "memory");
         advance(t, k);
       }
     }
@@ -321,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool row_ok = m0 + m < M;
     const int dim = (DIM > 0) ? DIM : kp.dim;
     float xr[DD];
+    float ai = 0.f;
     if constexpr (kGen) {
       // rows of every generated term of a group are the group's own points
       const float* xrp = nullptr;
@@ -331,6 +356,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 #pragma unroll
       for (int q = 0; q < DD; ++q) xr[q] = (xrp && row_ok && (DIM > 0 || q < dim)) ? xrp[size_t(m0 + m) * dim + q] : 0.f;
+      if constexpr (KIND == kGaussian) {
+        // -p0' |xi - xj|^2 = ai + bj + sum_q (2 p0' xi_q) xj_q with ai, bj the scaled norms
+        // (computed in FP64 at create): d + 1 FP32 ops per entry instead of 2d
+        const float* xrn = nullptr;
+        for (int t = grp.tbeg; t < grp.tend; ++t)
+          if (terms[t].flags & kTermGen) {
+            xrn = terms[t].xrn;
+            break;
+          }
+        ai = (xrn && row_ok) ? xrn[m0 + m] : 0.f;
+#pragma unroll
+        for (int q = 0; q < DD; ++q) xr[q] *= 2.f * kp.p0;
+      }
     }
     // drain state: this thread owns row em of the tile and columns [col0, col0 + BN/2)
     const int e = warp - kAWarp0;  // 0..7
@@ -364,19 +402,45 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (kGen) {
           float v[8];
           const int kb = k + 8 * h;
-          const float* xc = T.xc + size_t(kb) * dim;
+          // column coordinates of this stage (bulk-copied with the B tiles): broadcast LDS
+          mbar_wait(bar_full_b(st), (s / STAGES) & 1);
+          const uint32_t xs = x_tile(st) + uint32_t(8 * h * dim) * 4u;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            float acc = 0.f;
-            if constexpr (KIND == kPolynomial) {
+            float xc[DD];
+            if constexpr (DIM > 0 && DIM % 4 == 0) {
+#pragma unroll
+              for (int q = 0; q < DIM; q += 4) {
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                             : "=f"(xc[q]), "=f"(xc[q + 1]), "=f"(xc[q + 2]), "=f"(xc[q + 3])
+                             : "r"(xs + uint32_t(j * DIM + q) * 4u));
+              }
+            } else {
 #pragma unroll
               for (int q = 0; q < DD; ++q)
-                if (DIM > 0 || q < dim) acc = fmaf(xr[q], __ldg(xc + j * dim + q), acc);
+                if (DIM > 0 || q < dim)
+                  asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(xc[q]) : "r"(xs + uint32_t(j * dim + q) * 4u));
+            }
+            float acc = 0.f;
+            if constexpr (KIND == kGaussian) {
+              float bj;
+              asm volatile("ld.shared.f32 %0, [%1];\n"
+                           : "=f"(bj)
+                           : "r"(x_tile(st) + uint32_t(kBK * (kMaxDimRt + 1) * 4 + (8 * h + j) * 4)));
+              acc = ai + bj;
+#pragma unroll
+              for (int q = 0; q < DD; ++q)
+                if (DIM > 0 || q < dim) acc = fmaf(xr[q], xc[q], acc);
+              acc = fminf(acc, 0.f);  // d^2 >= 0 (rounding can make the expansion slightly positive)
+            } else if constexpr (KIND == kPolynomial) {
+#pragma unroll
+              for (int q = 0; q < DD; ++q)
+                if (DIM > 0 || q < dim) acc = fmaf(xr[q], xc[q], acc);
             } else {
 #pragma unroll
               for (int q = 0; q < DD; ++q)
                 if (DIM > 0 || q < dim) {
-                  const float e = xr[q] - __ldg(xc + j * dim + q);
+                  const float e = xr[q] - xc[q];
                   acc = fmaf(e, e, acc);
                 }
             }
@@ -483,6 +547,7 @@ cudaError_t launch_unpermute(const float* up, int64_t ldp, const int32_t* iperm,
                              int64_t ldu, cudaStream_t st);
 cudaError_t launch_split(const SplitJob* d_jobs, int njobs, float* hi, float* lo, cudaStream_t st);
 cudaError_t launch_to_f32(const double* x, int64_t n, float* y, cudaStream_t st);
+cudaError_t launch_scaled_norms(const double* x, int64_t npts, int dim, double scale, float* out, cudaStream_t st);
 
 }  // namespace f32
 }  // namespace gofmm

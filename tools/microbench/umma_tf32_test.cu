@@ -113,6 +113,15 @@ int run_case(const char* name, bool with_gen, int cpanel, int R, int M, int bigK
   CK(cudaMemcpy(dBh, Bh.data(), Bh.size() * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dBl, Bl.data(), Bl.size() * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dX, X.data(), X.size() * 4, cudaMemcpyHostToDevice));
+  std::vector<float> XN(rows);
+  for (int i = 0; i < rows; ++i) {
+    double s2 = 0;
+    for (int q = 0; q < D; ++q) s2 += double(X[size_t(i) * D + q]) * X[size_t(i) * D + q];
+    XN[i] = float(-p0d * 1.4426950408889634 * s2);
+  }
+  float* dXN;
+  CK(cudaMalloc(&dXN, XN.size() * 4));
+  CK(cudaMemcpy(dXN, XN.data(), XN.size() * 4, cudaMemcpyHostToDevice));
   std::vector<f32::Term> terms;
   std::vector<float*> keep;
   for (auto& t : ht) {
@@ -124,6 +133,8 @@ int run_case(const char* name, bool with_gen, int cpanel, int R, int M, int bigK
       T.flags = kTermGen;
       T.xr = dX;  // rows of the group = points [0, M)
       T.xc = dX + size_t(t.b_row) * D;
+      T.xrn = dXN;
+      T.xcn = dXN + t.b_row;
     } else {
       std::vector<float> ah(t.A.size()), al(t.A.size());
       for (size_t i = 0; i < t.A.size(); ++i) {

@@ -17,15 +17,17 @@ ap.add_argument("--budget", type=float, default=None)
 ap.add_argument("--evals", type=int, default=2)
 ap.add_argument("--far-mode", type=int, default=0)
 ap.add_argument("--near-mode", type=int, default=0)
+ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
 a = ap.parse_args()
 over = {"n": a.n}
 if a.budget is not None:
     over["budget"] = a.budget
 tree, cfg = synth.make_config_tree(a.config, **over)
-ev = Evaluator(tree, near_mode=a.near_mode, far_mode=a.far_mode)
+ev = Evaluator(tree, near_mode=a.near_mode, far_mode=a.far_mode, precision=a.precision)
 r = cfg["r"]
-w = torch.randn((r, tree.n), dtype=torch.float64, device="cuda").t()
-u = torch.empty((r, tree.n), dtype=torch.float64, device="cuda").t()
+dt = torch.float64 if a.precision == "fp64" else torch.float32
+w = torch.randn((r, tree.n), dtype=dt, device="cuda").t()
+u = torch.empty((r, tree.n), dtype=dt, device="cuda").t()
 for i in range(a.evals):
     _, st = ev.evaluate_torch(w, out=u, sync_stats=True)
     print(i, {k: round(v, 3) for k, v in st.items()}, ev.phase_flops(r), flush=True)
