@@ -259,14 +259,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     while (t < grp.tend && terms[t].K == 0) ++t;
     return t;
   };
-  auto advance = [&](int& t, int& k) {
-    k += kBK;
-    if (k >= terms[t].K) {
-      k = 0;
-      ++t;
-      while (t < grp.tend && terms[t].K == 0) ++t;
-    }
-  };
 
   // Each role branch runs to the kernel's end on its own (no code after the branches): setmaxnreg
   // gives every region its own register budget only if no code is shared across the two.
@@ -275,11 +267,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // =========================== B PRODUCER (TMA) ===========================
     if (lane == 0) {
+      // the current term lives in registers: every mbarrier wait clobbers memory, so a reference
+      // into `terms` would be re-read from global memory at every stage
       int t = first_term(), k = 0;
+      struct {
+        const float *xc, *xcn;
+        int64_t b_row;
+        int32_t K, flags, bbuf;
+      } T{};
+      auto load_term = [&]() {
+        if (t < grp.tend) {
+          T.xc = terms[t].xc;
+          T.xcn = terms[t].xcn;
+          T.b_row = terms[t].b_row;
+          T.K = terms[t].K;
+          T.flags = terms[t].flags;
+          T.bbuf = terms[t].bbuf;
+        }
+      };
+      load_term();
       for (int s = 0; s < total; ++s) {
         const int st = s % STAGES;
         mbar_wait(bar_empty(st), ((s / STAGES) & 1) ^ 1);
-        const Term& T = terms[t];
         const int32_t panel = int32_t((T.b_row + k) >> 4);
         // generated stage: the 16 column points' coordinates ride on the same barrier (one bulk
         // copy of 64*dim contiguous bytes; rows past K are padding points of the same buffer)
@@ -301,7 +310,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                   x_tile(st) + uint32_t(kBK * (kMaxDimRt + 1) * 4)),
               "l"(T.xcn + k), "r"(nbytes), "r"(bar_full_b(st))
               : "memory");
-        advance(t, k);
+        k += kBK;
+        if (k >= T.K) {
+          k = 0;
+          ++t;
+          while (t < grp.tend && terms[t].K == 0) ++t;
+          load_term();
+        }
       }
     }
   } else if (warp == 1) {
@@ -383,6 +398,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     int drained = 0;
     const uint32_t tq = tmem + (uint32_t(32 * q) << 16) + uint32_t(col0);
     int t = first_term(), k = 0;
+    // current term in registers (see the TMA thread): K, flags and the stored-A operand
+    int tK = 0, tFlags = 0;
+    const float* tAh = nullptr;
+    const float* tAl = nullptr;
+    int64_t tLda = 0;
+    auto load_term = [&]() {
+      if (t < grp.tend) {
+        tK = terms[t].K;
+        tFlags = terms[t].flags;
+        tAh = terms[t].a_hi;
+        tAl = terms[t].a_lo;
+        tLda = terms[t].lda;
+      }
+    };
+    load_term();
     int pending = -1;  // stage whose cp.async copies are still in flight (arrival deferred by one)
     auto arrive = [&](int st) {
       fence_proxy_async();  // generic-proxy writes -> visible to the tensor core (async proxy)
@@ -396,15 +426,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       // (its commit precedes or accompanies this stage's release, so the wait is short)
       if (s >= STAGES && (s - STAGES + 1) % kSeg == 0)
         drain_segment<BN, kHalf>(acc, drained++, tq, bar_tfull(0), bar_tempty(0), lane);
-      const Term& T = terms[t];
       const uint32_t dh = a_tile(st, 0), dl = a_tile(st, 1);
-      if (kGen && (T.flags & kTermGen)) {
+      if (kGen && (tFlags & kTermGen)) {
         if constexpr (kGen) {
           float v[8];
           const int kb = k + 8 * h;
+          const int nv = row_ok ? min(8, tK - kb) : 0;  // valid entries of this thread's 8
           // column coordinates of this stage (bulk-copied with the B tiles): broadcast LDS
           mbar_wait(bar_full_b(st), (s / STAGES) & 1);
           const uint32_t xs = x_tile(st) + uint32_t(8 * h * dim) * 4u;
+          float bn[8];  // scaled column norms (Gaussian)
+          if constexpr (KIND == kGaussian) {
+            const uint32_t xn = x_tile(st) + uint32_t(kBK * (kMaxDimRt + 1) * 4 + 32 * h);
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                         : "=f"(bn[0]), "=f"(bn[1]), "=f"(bn[2]), "=f"(bn[3]) : "r"(xn));
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                         : "=f"(bn[4]), "=f"(bn[5]), "=f"(bn[6]), "=f"(bn[7]) : "r"(xn + 16u));
+          }
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             float xc[DD];
@@ -423,11 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             float acc = 0.f;
             if constexpr (KIND == kGaussian) {
-              float bj;
-              asm volatile("ld.shared.f32 %0, [%1];\n"
-                           : "=f"(bj)
-                           : "r"(x_tile(st) + uint32_t(kBK * (kMaxDimRt + 1) * 4 + (8 * h + j) * 4)));
-              acc = ai + bj;
+              acc = ai + bn[j];
 #pragma unroll
               for (int q = 0; q < DD; ++q)
                 if (DIM > 0 || q < dim) acc = fmaf(xr[q], xc[q], acc);
@@ -444,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   acc = fmaf(e, e, acc);
                 }
             }
-            v[j] = (row_ok && kb + j < T.K) ? entry_from<KIND>(acc, kp) : 0.f;
+            v[j] = (j < nv) ? entry_from<KIND>(acc, kp) : 0.f;
           }
           float hi[8], lo[8];
 #pragma unroll
@@ -465,10 +499,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const int kc = k + 8 * h + 4 * c;
-          const bool v = row_ok && kc < T.K;
-          const size_t off = size_t(m0 + m) * T.lda + kc;
-          cp_async16(dh + sw64(m, 2 * h + c), v ? T.a_hi + off : T.a_hi, v);
-          cp_async16(dl + sw64(m, 2 * h + c), v ? T.a_lo + off : T.a_lo, v);
+          const bool v = row_ok && kc < tK;
+          const size_t off = size_t(m0 + m) * tLda + kc;
+          cp_async16(dh + sw64(m, 2 * h + c), v ? tAh + off : tAh, v);
+          cp_async16(dl + sw64(m, 2 * h + c), v ? tAl + off : tAl, v);
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
         if (pending >= 0) {
@@ -477,7 +511,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         pending = st;
       }
-      advance(t, k);
+      k += kBK;
+      if (k >= tK) {
+        k = 0;
+        ++t;
+        while (t < grp.tend && terms[t].K == 0) ++t;
+        load_term();
+      }
     }
     if (pending >= 0) {
       asm volatile("cp.async.wait_all;\n" ::: "memory");
