@@ -120,6 +120,19 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+// mbarrier wait that lets the hardware suspend the warp until the phase completes (bounded by
+// the hint, in ns) instead of spinning: spinning warps take issue slots from the generators
+__device__ __forceinline__ void mbar_sleep_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 // 32 lanes x 32 columns of FP32 from TMEM: thread t gets columns [col, col+32) of lane base+t
@@ -179,7 +192,7 @@ template <int BN, int NCOL>
 __device__ __forceinline__ void drain_segment(float (&acc)[NCOL], int seg, uint32_t tq, uint32_t tfull0,
                                               uint32_t tempty0, int lane) {
   const int b = seg & 1;
-  mbar_wait(tfull0 + 8u * b, (seg >> 1) & 1);
+  mbar_sleep_wait(tfull0 + 8u * b, (seg >> 1) & 1);
   tc_fence_after();
 #pragma unroll
   for (int cc = 0; cc < NCOL; cc += 32) {
@@ -288,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       load_term();
       for (int s = 0; s < total; ++s) {
         const int st = s % STAGES;
-        mbar_wait(bar_empty(st), ((s / STAGES) & 1) ^ 1);
+        mbar_sleep_wait(bar_empty(st), ((s / STAGES) & 1) ^ 1);
         const int32_t panel = int32_t((T.b_row + k) >> 4);
         // generated stage: the 16 column points' coordinates ride on the same barrier (one bulk
         // copy of 64*dim contiguous bytes; rows past K are padding points of the same buffer)
@@ -328,9 +341,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ph = (s / STAGES) & 1;
         const int seg = s / kSeg, b = seg & 1;
         const uint32_t dacc = tmem + uint32_t(b * BN);
-        if (s % kSeg == 0 && seg >= 2) mbar_wait(bar_tempty(b), ((seg >> 1) - 1) & 1);  // drained?
-        mbar_wait(bar_full_b(st), ph);
-        mbar_wait(bar_full_a(st), ph);
+        if (s % kSeg == 0 && seg >= 2) mbar_sleep_wait(bar_tempty(b), ((seg >> 1) - 1) & 1);  // drained?
+        mbar_sleep_wait(bar_full_b(st), ph);
+        mbar_sleep_wait(bar_full_a(st), ph);
         tc_fence_after();
         const uint64_t ah = desc_kmajor_sw64(a_tile(st, 0)), al = desc_kmajor_sw64(a_tile(st, 1));
         const uint64_t bh = desc_kmajor_sw64(b_tile(st, 0)), bl = desc_kmajor_sw64(b_tile(st, 1));
@@ -421,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     for (int s = 0; s < total; ++s) {
       const int st = s % STAGES;
-      mbar_wait(bar_empty(st), ((s / STAGES) & 1) ^ 1);
+      mbar_sleep_wait(bar_empty(st), ((s / STAGES) & 1) ^ 1);
       // the MMAs of stage s - STAGES have completed: once that closes a segment, drain it now
       // (its commit precedes or accompanies this stage's release, so the wait is short)
       if (s >= STAGES && (s - STAGES + 1) % kSeg == 0)
@@ -433,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int kb = k + 8 * h;
           const int nv = row_ok ? min(8, tK - kb) : 0;  // valid entries of this thread's 8
           // column coordinates of this stage (bulk-copied with the B tiles): broadcast LDS
-          mbar_wait(bar_full_b(st), (s / STAGES) & 1);
+          mbar_sleep_wait(bar_full_b(st), (s / STAGES) & 1);
           const uint32_t xs = x_tile(st) + uint32_t(8 * h * dim) * 4u;
           float bn[8];  // scaled column norms (Gaussian)
           if constexpr (KIND == kGaussian) {
@@ -465,7 +478,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int q = 0; q < DD; ++q)
                 if (DIM > 0 || q < dim) acc = fmaf(xr[q], xc[q], acc);
-              acc = fminf(acc, 0.f);  // d^2 >= 0 (rounding can make the expansion slightly positive)
             } else if constexpr (KIND == kPolynomial) {
 #pragma unroll
               for (int q = 0; q < DD; ++q)
@@ -478,7 +490,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                   acc = fmaf(e, e, acc);
                 }
             }
-            v[j] = (j < nv) ? entry_from<KIND>(acc, kp) : 0.f;
+            v[j] = entry_from<KIND>(acc, kp);
+          }
+          if (nv < 8) {  // ragged tail of a term / rows past M: zero (never taken mid-term)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = (j < nv) ? v[j] : 0.f;
           }
           float hi[8], lo[8];
 #pragma unroll
