@@ -331,6 +331,12 @@ struct gofmm_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
+  // host-buffer evaluation pipeline (evaluate_host): H2D / D2H copy streams and, per staging
+  // buffer b, events in_ready / comp_done / out_free and copy-timing pairs
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t pev[2][3] = {};
+  cudaEvent_t tev[2][4] = {};
+  gofmm::DevBuf d_win2[2], d_uout2[2];
   std::vector<cudaEvent_t> lev;  // per-launch start/stop events (timed evaluations only)
   std::vector<float> launch_ms;  // durations of the last timed evaluation (summed over chunks)
   float phase_ms[4] = {0, 0, 0, 0};
@@ -1570,6 +1576,14 @@ int gofmm_destroy(gofmm_handle* H) {
     for (auto& e : H->lev)
       if (e) cudaEventDestroy(e);
     if (H->stream) cudaStreamDestroy(H->stream);
+    for (auto* st : {H->s_h2d, H->s_d2h})
+      if (st) cudaStreamDestroy(st);
+    for (auto& row : H->pev)
+      for (auto& e : row)
+        if (e) cudaEventDestroy(e);
+    for (auto& row : H->tev)
+      for (auto& e : row)
+        if (e) cudaEventDestroy(e);
     delete H;
   });
 }
@@ -1609,7 +1623,7 @@ int64_t gofmm_device_bytes(const gofmm_handle* H) {
   const DevBuf* bufs[] = {&H->d_proj, &H->d_diag, &H->d_near,  &H->d_far,   &H->d_xp,   &H->d_xs,
                           &H->d_prow, &H->d_iperm, &H->d_tiles, &H->d_groups, &H->d_terms, &H->d_wp,
                           &H->d_what, &H->d_c,    &H->d_win,   &H->d_uout, &H->d_a32h, &H->d_a32l,
-                          &H->d_xp32, &H->d_xs32, &H->d_xpn32, &H->d_xsn32, &H->d_terms32, &H->d_tiles32, &H->d_wp32[0], &H->d_wp32[1],
+                          &H->d_win2[0], &H->d_win2[1], &H->d_uout2[0], &H->d_uout2[1], &H->d_xp32, &H->d_xs32, &H->d_xpn32, &H->d_xsn32, &H->d_terms32, &H->d_tiles32, &H->d_wp32[0], &H->d_wp32[1],
                           &H->d_what32[0], &H->d_what32[1], &H->d_c32[0], &H->d_c32[1], &H->d_win32, &H->d_uout32};
   int64_t s = 0;
   for (auto* b : bufs) s += int64_t(b->bytes);
@@ -1644,54 +1658,91 @@ namespace {
 template <class T>
 void evaluate_host(gofmm_handle* H, const T* w, int64_t ldw, int32_t r, T* u_perm, int64_t ldu,
                    gofmm_eval_stats* stats) {
+  // Column chunks flow through a 3-stream pipeline (evaluation is column-separable):
+  // H2D of chunk i+1 (copy stream 1) and D2H of chunk i-1 (copy stream 2) overlap the
+  // evaluation of chunk i (the handle's stream), with two staging buffers for W and u. Only the
+  // first upload and the last download are exposed.
   constexpr bool kF32 = sizeof(T) == 4;
   check_args(H, w, ldw, r, u_perm, ldu);
   check_precision(H, kF32 ? GOFMM_PRECISION_F32 : GOFMM_PRECISION_F64);
   GOFMM_CUDA(cudaSetDevice(H->device));
   auto t0 = std::chrono::steady_clock::now();
   cudaStream_t st = H->stream;
-  DevBuf& win = kF32 ? H->d_win32 : H->d_win;
-  DevBuf& uout = kF32 ? H->d_uout32 : H->d_uout;
-  // device staging for W and u (a column chunk at a time when r does not fit)
-  const int32_t rc_ws = kF32 ? rhs_chunk32(H, r) : rhs_chunk(H, r);
-  size_t free_b = 0, total_b = 0;
-  GOFMM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const size_t per_col = size_t(H->n) * sizeof(T);
-  int32_t rc = std::min<int32_t>(
-      r, std::max<int32_t>(1, int32_t(std::min<size_t>(size_t(rc_ws), (free_b / 2 + win.bytes) / (2 * per_col)))));
-  const size_t bytes = per_col * size_t(rc);
-  if (win.bytes < bytes) {
-    win.alloc(bytes, false);
-    uout.alloc(bytes, false);
+  if (!H->s_h2d) {
+    GOFMM_CUDA(cudaStreamCreateWithFlags(&H->s_h2d, cudaStreamNonBlocking));
+    GOFMM_CUDA(cudaStreamCreateWithFlags(&H->s_d2h, cudaStreamNonBlocking));
+    for (auto& row : H->pev)
+      for (auto& e : row) GOFMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& row : H->tev)
+      for (auto& e : row) GOFMM_CUDA(cudaEventCreate(&e));
   }
+  // chunk: one 256-column N tile (both kernel families tile 256 columns) unless r is smaller or
+  // the workspace forces less
+  const int32_t rc_ws = kF32 ? rhs_chunk32(H, r) : rhs_chunk(H, r);
+  const int32_t rc = std::max<int32_t>(1, std::min<int32_t>({r, rc_ws, r > 256 ? 256 : r}));
+  const size_t per_col = size_t(H->n) * sizeof(T);
+  const size_t bytes = per_col * size_t(rc);
+  for (int b = 0; b < 2; ++b)
+    if (H->d_win2[b].bytes < bytes) {
+      H->d_win2[b].alloc(bytes, false);
+      H->d_uout2[b].alloc(bytes, false);
+    }
   float h2d = 0, d2h = 0, ph[4] = {0, 0, 0, 0};
   std::vector<float> lms(H->launches.size(), 0.f);
-  for (int32_t c0 = 0; c0 < r; c0 += rc) {
-    const int32_t rr = std::min(rc, r - c0);
-    GOFMM_CUDA(cudaEventRecord(H->ev[5], st));
-    GOFMM_CUDA(cudaMemcpy2DAsync(win.p, per_col, w + size_t(c0) * ldw, size_t(ldw) * sizeof(T), per_col, rr,
-                                 cudaMemcpyHostToDevice, st));
-    GOFMM_CUDA(cudaEventRecord(H->ev[6], st));
+  const int nchunks = int((r + rc - 1) / rc);
+  auto h2d_copy = [&](int i) {
+    const int b = i & 1;
+    const int32_t c0 = i * rc, rr = std::min(rc, r - c0);
+    // the buffer's previous chunk (i - 2) must have been consumed by its evaluation
+    if (i >= 2) GOFMM_CUDA(cudaStreamWaitEvent(H->s_h2d, H->pev[b][1], 0));
+    if (stats) GOFMM_CUDA(cudaEventRecord(H->tev[b][0], H->s_h2d));
+    GOFMM_CUDA(cudaMemcpy2DAsync(H->d_win2[b].p, per_col, w + size_t(c0) * ldw, size_t(ldw) * sizeof(T), per_col,
+                                 rr, cudaMemcpyHostToDevice, H->s_h2d));
+    if (stats) GOFMM_CUDA(cudaEventRecord(H->tev[b][1], H->s_h2d));
+    GOFMM_CUDA(cudaEventRecord(H->pev[b][0], H->s_h2d));  // in_ready
+  };
+  if (nchunks > 0) h2d_copy(0);
+  for (int i = 0; i < nchunks; ++i) {
+    const int b = i & 1;
+    const int32_t c0 = i * rc, rr = std::min(rc, r - c0);
+    if (i + 1 < nchunks) h2d_copy(i + 1);  // prefetch the next chunk before evaluating this one
+    GOFMM_CUDA(cudaStreamWaitEvent(st, H->pev[b][0], 0));            // W chunk landed
+    if (i >= 2) GOFMM_CUDA(cudaStreamWaitEvent(st, H->pev[b][2], 0));  // u buffer downloaded
     if constexpr (kF32)
-      enqueue32(H, win.as<float>(), H->n, rr, uout.as<float>(), H->n, st, stats != nullptr);
+      enqueue32(H, H->d_win2[b].as<float>(), H->n, rr, H->d_uout2[b].as<float>(), H->n, st, stats != nullptr);
     else
-      enqueue(H, win.as<double>(), H->n, rr, uout.as<double>(), H->n, st, stats != nullptr);
-    GOFMM_CUDA(cudaEventRecord(H->ev[4], st));
-    GOFMM_CUDA(cudaMemcpy2DAsync(u_perm + size_t(c0) * ldu, size_t(ldu) * sizeof(T), uout.p, per_col, per_col, rr,
-                                 cudaMemcpyDeviceToHost, st));
-    GOFMM_CUDA(cudaEventRecord(H->ev[7], st));
-    GOFMM_CUDA(cudaStreamSynchronize(st));
+      enqueue(H, H->d_win2[b].as<double>(), H->n, rr, H->d_uout2[b].as<double>(), H->n, st, stats != nullptr);
+    GOFMM_CUDA(cudaEventRecord(H->pev[b][1], st));  // comp_done: W buffer free, u chunk ready
+    GOFMM_CUDA(cudaStreamWaitEvent(H->s_d2h, H->pev[b][1], 0));
+    if (stats) GOFMM_CUDA(cudaEventRecord(H->tev[b][2], H->s_d2h));
+    GOFMM_CUDA(cudaMemcpy2DAsync(u_perm + size_t(c0) * ldu, size_t(ldu) * sizeof(T), H->d_uout2[b].p, per_col,
+                                 per_col, rr, cudaMemcpyDeviceToHost, H->s_d2h));
+    if (stats) GOFMM_CUDA(cudaEventRecord(H->tev[b][3], H->s_d2h));
+    GOFMM_CUDA(cudaEventRecord(H->pev[b][2], H->s_d2h));  // out_free
     if (stats) {
-      float a, b;
-      GOFMM_CUDA(cudaEventElapsedTime(&a, H->ev[5], H->ev[6]));
-      GOFMM_CUDA(cudaEventElapsedTime(&b, H->ev[4], H->ev[7]));
+      // enqueue() synchronised on this chunk's evaluation; collect its copy times when the
+      // buffer is reused (or at the end)
+      for (int p = 0; p < 4; ++p) ph[p] += H->phase_ms[p];
+      for (size_t k = 0; k < lms.size(); ++k) lms[k] += H->launch_ms[k];
+    }
+    if (stats && i >= 1) {  // chunk i-1's copies are complete once its D2H event is
+      const int pb = (i - 1) & 1;
+      GOFMM_CUDA(cudaEventSynchronize(H->tev[pb][3]));
+      float a, c;
+      GOFMM_CUDA(cudaEventElapsedTime(&a, H->tev[pb][0], H->tev[pb][1]));
+      GOFMM_CUDA(cudaEventElapsedTime(&c, H->tev[pb][2], H->tev[pb][3]));
       h2d += a;
-      d2h += b;
-      for (int i = 0; i < 4; ++i) ph[i] += H->phase_ms[i];
-      for (size_t i = 0; i < lms.size(); ++i) lms[i] += H->launch_ms[i];
+      d2h += c;
     }
   }
+  GOFMM_CUDA(cudaStreamSynchronize(H->s_d2h));
   if (stats) {
+    const int lb = (nchunks - 1) & 1;
+    float a, c;
+    GOFMM_CUDA(cudaEventElapsedTime(&a, H->tev[lb][0], H->tev[lb][1]));
+    GOFMM_CUDA(cudaEventElapsedTime(&c, H->tev[lb][2], H->tev[lb][3]));
+    h2d += a;
+    d2h += c;
     std::memset(stats, 0, sizeof(*stats));
     stats->flops = H->flops_per_rhs * int64_t(r);
     std::copy(ph, ph + 4, H->phase_ms);
