@@ -397,16 +397,19 @@ def dist_arm(args, world, rank, local):
     tree, cfg = synth.make_config_tree(args.config, seed=args.seed, **{k: cfg[k] for k in ("n", "budget")})
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
-    ev = Evaluator(tree, device=local, rank=rank, nranks=world)
+    f32 = args.precision == "fp32"
+    tdt = torch.float32 if f32 else torch.float64
+    esz = 4 if f32 else 8
+    ev = Evaluator(tree, device=local, rank=rank, nranks=world, precision=args.precision)
     t_create = time.perf_counter() - t0
     info = ev.dist_info()
     full_flops = info["full_flops_per_rhs"] * r
     gen = torch.Generator(device="cuda").manual_seed(1000)  # every rank holds the same W
-    w = torch.randn((r, tree.n), dtype=torch.float64, device="cuda", generator=gen).t()
-    u = torch.zeros((r, tree.n), dtype=torch.float64, device="cuda").t()
-    slot = info["max_send_rows"] * r
-    send = torch.empty(slot, dtype=torch.float64, device="cuda")
-    recv = torch.empty(slot * world, dtype=torch.float64, device="cuda")
+    w = torch.randn((r, tree.n), dtype=tdt, device="cuda", generator=gen).t()
+    u = torch.zeros((r, tree.n), dtype=tdt, device="cuda").t()
+    slot = ev.send_elems(r)
+    send = torch.empty(slot, dtype=tdt, device="cuda")
+    recv = torch.empty(slot * world, dtype=tdt, device="cuda")
 
     def step():
         ev.dist_stage1_torch(w, send)
@@ -430,15 +433,15 @@ def dist_arm(args, world, rank, local):
         barrier(world)
     ms = allmax(e0.elapsed_time(e1) / args.steps, world)
     value = full_flops / (ms * 1e-3) / 1e9
-    peak, peak_src = fp64_peak_tflops()
+    peak, peak_src = tf32x3_peak_tflops() if f32 else fp64_peak_tflops()
 
     # end to end: pinned host W -> device, evaluation, own rows of u -> pinned host
     e2e = None
     if not args.no_e2e:
-        w_h = torch.empty((r, tree.n), dtype=torch.float64, pin_memory=True)
+        w_h = torch.empty((r, tree.n), dtype=tdt, pin_memory=True)
         w_h.copy_(w.t())
         own = slice(int(info["own_row_begin"]), int(info["own_row_end"]))
-        u_h = torch.empty((r, own.stop - own.start), dtype=torch.float64, pin_memory=True)
+        u_h = torch.empty((r, own.stop - own.start), dtype=tdt, pin_memory=True)
         ts = []
         for it in range(args.e2e_steps + 1):
             barrier(world)
@@ -452,19 +455,20 @@ def dist_arm(args, world, rank, local):
                 ts.append(time.perf_counter() - t1)
         sec = allmax(float(np.mean(ts)), world)
         e2e = {"value": round(full_flops / sec / 1e9, 3), "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(tree.n * r * 8), "d2h_bytes_per_step": int((own.stop - own.start) * r * 8),
+               "h2d_bytes_per_step": int(tree.n * r * esz), "d2h_bytes_per_step": int((own.stop - own.start) * r * esz),
                "sec_per_eval": round(sec, 5), "note": "per rank: full W in, own rows of u out"}
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f32" if f32 else "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {KERNEL_NAMES.get(cfg['kernel'], 'kernel')} h={cfg['h']} N={tree.n} "
                                f"d={cfg['d']} m={cfg['m']} s={cfg['s']} budget={cfg['budget']} r={r} total",
                    "n": tree.n, "r": r, "budget": cfg["budget"], "parallelism": f"subtree split x{world}",
-                   "split_level": info["split_level"], "allgather_bytes_per_rank": int(slot * 8),
-                   "l2_flush": f"inputs larger than L2 (W {tree.n * r * 8 / 1e9:.2f} GB)"},
+                   "split_level": info["split_level"], "allgather_bytes_per_rank": int(slot * esz),
+                   "l2_flush": f"inputs larger than L2 (W {tree.n * r * esz / 1e9:.2f} GB)",
+                   "precision": args.precision},
         "sec_per_eval": round(ms / 1e3, 6),
-        "pct_fp64_peak": round(100.0 * value / 1e3 / (peak * world), 2),
+        ("pct_3xtf32_peak" if f32 else "pct_fp64_peak"): round(100.0 * value / 1e3 / (peak * world), 2),
         "flops_per_eval": int(full_flops),
         "rank_flops_max": int(allmax(float(info["flops_per_rhs"] * r), world)),
         "rel_error": None,
@@ -504,8 +508,6 @@ def main():
     if args.impl == "reference":
         rc = reference_arm(args, world, rank)
     elif world > 1 or args.dist:
-        if args.precision != "fp64":
-            raise SystemExit("the subtree-split (multi-GPU) path is fp64 only")
         rc = dist_arm(args, world, rank, local)
     else:
         rc = ours_arm(args, world, rank, local)

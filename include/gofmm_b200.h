@@ -204,6 +204,12 @@ int gofmm_dist_stage1(gofmm_handle* h, const double* d_w, int64_t ldw, int32_t r
 /* d_recv: nranks x max_send_rows x r doubles (all-gathered); writes u_perm rows of this rank. */
 int gofmm_dist_stage2(gofmm_handle* h, const double* d_recv, int32_t r, double* d_u_perm, int64_t ldu, void* stream);
 
+/* FP32 handles: the same two stages; the send buffer is 2 * max_send_rows * r floats (hi then
+ * lo halves of the 3xTF32 operands), recv is nranks of those slots in rank order. */
+int gofmm_dist_stage1_f32(gofmm_handle* h, const float* d_w, int64_t ldw, int32_t r, float* d_send, void* stream);
+int gofmm_dist_stage2_f32(gofmm_handle* h, const float* d_recv, int32_t r, float* d_u_perm, int64_t ldu,
+                          void* stream);
+
 /* ---- error_eps2 support (evaluate.hpp:330-373) ---------------------------------------------
  * Exact rows of K W for nrows ORIGINAL indices `rows` (host array), W on the device in original
  * order; out is nrows x r column-major (device). Matrix-free kernel sources only. */

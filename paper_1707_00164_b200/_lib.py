@@ -132,7 +132,7 @@ EXPORTS = ("gofmm_create", "gofmm_evaluate", "gofmm_evaluate_device", "gofmm_unp
            "gofmm_last_error", "gofmm_abi_version", "gofmm_create_dist", "gofmm_dist_get_info",
            "gofmm_dist_plan_host", "gofmm_dist_stage1", "gofmm_dist_stage2", "gofmm_exact_rows",
            "gofmm_rng_eps2_draw", "gofmm_evaluate_f32", "gofmm_evaluate_device_f32",
-           "gofmm_unpermute_device_f32", "gofmm_precision")
+           "gofmm_unpermute_device_f32", "gofmm_precision", "gofmm_dist_stage1_f32", "gofmm_dist_stage2_f32")
 
 
 def lib():
@@ -161,6 +161,8 @@ def lib():
         L.gofmm_dist_plan_host.argtypes = [C.POINTER(TreeDesc), C.c_int32, C.c_int32, C.POINTER(DistInfo), C.c_int32, P]
         L.gofmm_dist_stage1.argtypes = [P, P, C.c_int64, C.c_int32, P, P]
         L.gofmm_dist_stage2.argtypes = [P, P, C.c_int32, P, C.c_int64, P]
+        L.gofmm_dist_stage1_f32.argtypes = [P, P, C.c_int64, C.c_int32, P, P]
+        L.gofmm_dist_stage2_f32.argtypes = [P, P, C.c_int32, P, C.c_int64, P]
         L.gofmm_exact_rows.argtypes = [P, P, C.c_int32, P, C.c_int64, C.c_int32, P, C.c_int64, P]
         L.gofmm_rng_eps2_draw.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, P, P, C.c_int64]
         L.gofmm_device_bytes.argtypes = [P]

@@ -442,7 +442,6 @@ void validate(const gofmm_tree_desc* d) {
 int f32_bn(int32_t r) { return r > 128 ? 256 : r > 64 ? 128 : 64; }
 
 void build_f32(gofmm_handle* H) {
-  if (H->nranks > 1) throw Error(GOFMM_ERR_INVALID, "fp32 precision: single-GPU handles only");
   const double* blobs[4] = {H->d_proj.as<double>(), H->d_diag.as<double>(), H->d_near.as<double>(),
                             H->d_far.as<double>()};
   struct Key {
@@ -1320,8 +1319,10 @@ void encode_bmap32(CUtensorMap* map, const float* ptr, int64_t rows, int32_t r, 
   if (rc != CUDA_SUCCESS) throw Error(GOFMM_ERR_CUDA, "cuTensorMapEncodeTiled (fp32) failed: " + std::to_string(int(rc)));
 }
 
+// stage 0: the whole evaluation; stage 1 / 2: the distributed halves around the all-gather
+// (d_xbuf = this rank's send buffer / the gathered receive buffer, hi/lo slots, see panel_copy_f32)
 void enqueue_chunk32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, float* d_u, int64_t ldu,
-                     cudaStream_t st, bool timed) {
+                     cudaStream_t st, bool timed, int stage = 0, float* d_xbuf = nullptr) {
   ensure_workspace32(H, r);
   const int bn = f32_bn(r);
   if (H->k32_s.bn != bn) {
@@ -1341,11 +1342,19 @@ void enqueue_chunk32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, 
   }
   const int64_t pstride = int64_t(H->ws32_r) * 16;
   if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[0], st));
-  GOFMM_CUDA(f32::launch_permute_in(d_w, ldw, H->d_prow.as<int32_t>(), 0, H->ld_wp, r, H->n, H->d_wp32[0].as<float>(),
-                                    H->d_wp32[1].as<float>(), pstride, st));
+  if (stage == 2 && H->n_unpack > 0)  // ghosts: other ranks' exported what / W rows
+    GOFMM_CUDA(f32::launch_panel_copy(H->d_segs.as<PanelSeg>() + H->n_pack, H->n_unpack, H->d_what32[0].as<float>(),
+                                      H->d_what32[1].as<float>(), H->d_wp32[0].as<float>(), H->d_wp32[1].as<float>(),
+                                      pstride, d_xbuf, r, H->dist.max_send_rows, 0, st));
+  if (stage != 2) {
+    const int64_t row0 = stage == 1 ? H->own_pst_begin : 0, row1 = stage == 1 ? H->own_pst_end : H->ld_wp;
+    GOFMM_CUDA(f32::launch_permute_in(d_w, ldw, H->d_prow.as<int32_t>(), row0, row1, r, H->n,
+                                      H->d_wp32[0].as<float>(), H->d_wp32[1].as<float>(), pstride, st));
+  }
   if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[1], st));
   int marked = 1;
   for (const Launch& L : H->launches) {
+    if (stage != 0 && L.stage != stage) continue;
     while (timed && marked <= L.phase) GOFMM_CUDA(cudaEventRecord(H->ev[1 + marked++], st));
     float *ch, *cl;
     int64_t ldc;
@@ -1363,6 +1372,10 @@ void enqueue_chunk32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, 
                                 st));
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li + 1], st));
   }
+  if (stage == 1 && H->n_pack > 0)
+    GOFMM_CUDA(f32::launch_panel_copy(H->d_segs.as<PanelSeg>(), H->n_pack, H->d_what32[0].as<float>(),
+                                      H->d_what32[1].as<float>(), H->d_wp32[0].as<float>(), H->d_wp32[1].as<float>(),
+                                      pstride, d_xbuf, r, H->dist.max_send_rows, 1, st));
   if (timed) {
     while (marked <= 2) GOFMM_CUDA(cudaEventRecord(H->ev[1 + marked++], st));
     GOFMM_CUDA(cudaEventRecord(H->ev[4], st));
@@ -1563,6 +1576,29 @@ int gofmm_dist_stage2(gofmm_handle* H, const double* d_recv, int32_t r, double* 
     GOFMM_CUDA(cudaSetDevice(H->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
     enqueue_chunk(H, nullptr, H->n, r, d_u, ldu, st, false, 2, const_cast<double*>(d_recv));
+  });
+}
+
+int gofmm_dist_stage1_f32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, float* d_send, void* stream) {
+  return guarded([&] {
+    check_args(H, d_w, ldw, r, d_w, H->n);
+    check_precision(H, GOFMM_PRECISION_F32);
+    if (H->nranks > 1 && !d_send && H->dist.max_send_rows > 0) throw Error(GOFMM_ERR_INVALID, "null send buffer");
+    GOFMM_CUDA(cudaSetDevice(H->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    enqueue_chunk32(H, d_w, ldw, r, nullptr, H->n, st, false, 1, d_send);
+  });
+}
+
+int gofmm_dist_stage2_f32(gofmm_handle* H, const float* d_recv, int32_t r, float* d_u, int64_t ldu, void* stream) {
+  return guarded([&] {
+    check_args(H, d_u, H->n, r, d_u, ldu);
+    check_precision(H, GOFMM_PRECISION_F32);
+    if (H->nranks > 1 && !d_recv && H->dist.max_send_rows > 0) throw Error(GOFMM_ERR_INVALID, "null receive buffer");
+    if (r > H->ws32_r) throw Error(GOFMM_ERR_INVALID, "stage2: r differs from stage1");
+    GOFMM_CUDA(cudaSetDevice(H->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    enqueue_chunk32(H, nullptr, H->n, r, d_u, ldu, st, false, 2, const_cast<float*>(d_recv));
   });
 }
 

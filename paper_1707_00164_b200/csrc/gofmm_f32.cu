@@ -70,6 +70,34 @@ static __global__ void scaled_norms(const double* __restrict__ x, int64_t npts, 
   }
 }
 
+// Subtree-split exchange (FP32): whole 16-row panels (first r columns, hi and lo) between the
+// workspace and the exchange buffer. Each rank's slot holds slot_rows x r hi floats followed by
+// slot_rows x r lo floats; a segment's buf_row = slot * slot_rows + offset in the slot.
+static __global__ void panel_copy_f32(const PanelSeg* __restrict__ segs, float* __restrict__ what_h,
+                                      float* __restrict__ what_l, float* __restrict__ wp_h, float* __restrict__ wp_l,
+                                      int64_t ws_pstride, float* __restrict__ buf, int32_t r, int64_t slot_rows,
+                                      int32_t to_buffer) {
+  const PanelSeg sg = segs[blockIdx.x];
+  const int64_t npan = sg.rows / 16;
+  const int64_t per = int64_t(16) * r;
+  const int64_t slot = sg.buf_row / slot_rows, off = sg.buf_row % slot_rows;
+  float* bh = buf + slot * 2 * slot_rows * r + (off / 16) * per;
+  float* bl = bh + slot_rows * r;
+  float* wh = (sg.buf == 0 ? what_h : wp_h) + (sg.ws_row / 16) * ws_pstride;
+  float* wl = (sg.buf == 0 ? what_l : wp_l) + (sg.ws_row / 16) * ws_pstride;
+  for (int64_t p = blockIdx.y; p < npan; p += gridDim.y) {
+    for (int64_t i = threadIdx.x; i < per; i += blockDim.x) {
+      if (to_buffer) {
+        bh[p * per + i] = wh[p * ws_pstride + i];
+        bl[p * per + i] = wl[p * ws_pstride + i];
+      } else {
+        wh[p * ws_pstride + i] = bh[p * per + i];
+        wl[p * ws_pstride + i] = bl[p * per + i];
+      }
+    }
+  }
+}
+
 template <int BN>
 constexpr int stages_for() {
   return BN == 256 ? 4 : BN == 128 ? 6 : 8;  // ~192 KB of pipeline in every configuration
@@ -154,6 +182,15 @@ cudaError_t launch_split(const SplitJob* d_jobs, int njobs, float* hi, float* lo
 cudaError_t launch_scaled_norms(const double* x, int64_t npts, int dim, double scale, float* out, cudaStream_t st) {
   if (npts <= 0) return cudaSuccess;
   scaled_norms<<<unsigned(std::min<int64_t>((npts + 255) / 256, 4096)), 256, 0, st>>>(x, npts, dim, scale, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_panel_copy(const PanelSeg* segs, int nseg, float* what_h, float* what_l, float* wp_h, float* wp_l,
+                              int64_t ws_pstride, float* buf, int32_t r, int64_t slot_rows, int32_t to_buffer,
+                              cudaStream_t st) {
+  if (nseg <= 0) return cudaSuccess;
+  dim3 grid(unsigned(nseg), 8);
+  panel_copy_f32<<<grid, 256, 0, st>>>(segs, what_h, what_l, wp_h, wp_l, ws_pstride, buf, r, slot_rows, to_buffer);
   return cudaGetLastError();
 }
 

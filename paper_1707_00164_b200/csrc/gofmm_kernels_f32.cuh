@@ -603,6 +603,9 @@ cudaError_t launch_unpermute(const float* up, int64_t ldp, const int32_t* iperm,
                              int64_t ldu, cudaStream_t st);
 cudaError_t launch_split(const SplitJob* d_jobs, int njobs, float* hi, float* lo, cudaStream_t st);
 cudaError_t launch_to_f32(const double* x, int64_t n, float* y, cudaStream_t st);
+cudaError_t launch_panel_copy(const PanelSeg* segs, int nseg, float* what_h, float* what_l, float* wp_h, float* wp_l,
+                              int64_t ws_pstride, float* buf, int32_t r, int64_t slot_rows, int32_t to_buffer,
+                              cudaStream_t st);
 cudaError_t launch_scaled_norms(const double* x, int64_t npts, int dim, double scale, float* out, cudaStream_t st);
 
 }  // namespace f32

@@ -282,13 +282,18 @@ class Evaluator:
         L.check(L.lib().gofmm_dist_get_info(self._h, C.byref(info)))
         return info.as_dict()
 
+    def send_elems(self, r: int) -> int:
+        """Elements of this rank's all-gather slot: max_send_rows x r (FP64), twice that (FP32 hi/lo)."""
+        return self.dist_info()["max_send_rows"] * r * (1 if self.precision == "fp64" else 2)
+
     def dist_stage1_torch(self, w, send):
         """Own-subtree upward pass + pack of this rank's exports into `send` (CUDA float64)."""
         import torch
 
         wt = _colmajor(w)
         stream = torch.cuda.current_stream(w.device).cuda_stream
-        L.check(L.lib().gofmm_dist_stage1(self._h, C.c_void_p(wt.data_ptr()), wt.stride(1), int(w.shape[1]),
+        fn = L.lib().gofmm_dist_stage1 if self.precision == "fp64" else L.lib().gofmm_dist_stage1_f32
+        L.check(fn(self._h, C.c_void_p(wt.data_ptr()), wt.stride(1), int(w.shape[1]),
                                           C.c_void_p(send.data_ptr()) if send.numel() else None,
                                           C.c_void_p(stream if stream else 1)))
 
@@ -297,7 +302,8 @@ class Evaluator:
         import torch
 
         stream = torch.cuda.current_stream(out.device).cuda_stream
-        L.check(L.lib().gofmm_dist_stage2(self._h, C.c_void_p(recv.data_ptr()) if recv.numel() else None, r,
+        fn = L.lib().gofmm_dist_stage2 if self.precision == "fp64" else L.lib().gofmm_dist_stage2_f32
+        L.check(fn(self._h, C.c_void_p(recv.data_ptr()) if recv.numel() else None, r,
                                           C.c_void_p(out.data_ptr()), out.stride(1),
                                           C.c_void_p(stream if stream else 1)))
 
@@ -308,7 +314,7 @@ class Evaluator:
 
         info = self.dist_info()
         r = int(w.shape[1])
-        send = torch.empty(info["max_send_rows"] * r, dtype=torch.float64, device=w.device)
+        send = torch.empty(self.send_elems(r), dtype=w.dtype, device=w.device)
         self.dist_stage1_torch(w, send)
         recv = all_gather(send)
         self.dist_stage2_torch(recv, r, out)

@@ -179,3 +179,44 @@ def test_f32_eps2_close_to_reference(gpu, oracle):
     with gpu.Evaluator(to_tree(h.export()), precision="fp32") as ev:
         rep = ev.error_eps2(1, 100, 42)
     assert abs(rep["eps2"] - rep_ref["eps2"]) <= 1e-4 * rep_ref["eps2"]
+
+
+def simulate_subtree_split32(G, tree, w_np, nranks):
+    """All nranks of the FP32 subtree-split evaluation on ONE device (see test_parity_gpu.py):
+    stage1 per rank, the all-gather as a concatenation of the hi/lo send slots, stage2 per rank."""
+    import torch
+
+    r = w_np.shape[1]
+    evs = [G.Evaluator(tree, rank=g, nranks=nranks, precision="fp32") for g in range(nranks)]
+    slot = evs[0].send_elems(r)
+    w = torch.from_numpy(np.ascontiguousarray(w_np.T.astype(np.float32))).cuda().t()
+    sends = [torch.zeros(slot, dtype=torch.float32, device="cuda") for _ in evs]
+    for e, sb in zip(evs, sends):
+        e.dist_stage1_torch(w, sb)
+    recv = torch.cat(sends) if slot else torch.zeros(0, dtype=torch.float32, device="cuda")
+    u = torch.full((r, tree.n), float("nan"), dtype=torch.float32, device="cuda").t()
+    for e in evs:
+        e.dist_stage2_torch(recv, r, u)
+    torch.cuda.synchronize()
+    out = u.cpu().numpy()
+    for e in evs:
+        e.close()
+    return out
+
+
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+def test_f32_subtree_split_matches_single_gpu(gpu, oracle, nranks):
+    """north_star (4) in FP32: subtree split + one all-gather equals the single-GPU FP32 result
+    and stays within 1e-5 of the reference FP64 evaluate."""
+    from paper_1707_00164_b200 import synth
+
+    tree, _ = synth.make_config_tree("c3", n=1 << 15, seed=1)
+    w = np.asfortranarray(np.random.default_rng(5).standard_normal((tree.n, 24)))
+    ref = oracle.import_flat(tree, threads=8)
+    u_ref, _, _ = ref.evaluate(w, threads=8)
+    with gpu.Evaluator(tree, precision="fp32") as ev:
+        single = ev.evaluate(w.astype(np.float32)).u
+    u = simulate_subtree_split32(gpu, tree, w, nranks)
+    assert not np.isnan(u).any(), "some rows of u were not written by their owner"
+    assert rel2(u.astype(np.float64), single.astype(np.float64)) <= 1e-6
+    assert rel2(u.astype(np.float64), u_ref) <= TOL32
