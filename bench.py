@@ -304,6 +304,9 @@ def ours_arm(args, world, rank, local):
     if not args.no_e2e:
         w_h = torch.empty((r, tree.n), dtype=tdt, pin_memory=True)
         w_h.copy_(w.t())
+        # the host-API leg owns the HBM a user's call would have: drop the device-resident W / u
+        del w, u, flush
+        torch.cuda.empty_cache()
         u_h = torch.empty((r, tree.n), dtype=tdt, pin_memory=True)
         wn, un = w_h.numpy().T, u_h.numpy().T  # Fortran-ordered N x r views of pinned memory
         ev.evaluate(wn, out=un)  # warm

@@ -29,6 +29,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -92,12 +93,17 @@ struct DevBuf {
 // ---------------------------------------------------------------- kernel configurations
 // S: stored-operand GEMMs (N2S / downward / output without generation): 128x128 CTA tile,
 //    8 consumer warps of 32x64.
-// G: generated-operand GEMMs (matrix-free L2L and S2S): 64x256 CTA tile, 8 consumer warps of
-//    8x256 — warps split M only, so every A entry is generated exactly once per CTA, and BN is
-//    wide to amortise exp() over the RHS columns.
+// G: generated-operand GEMMs (matrix-free L2L and S2S), r <= 256: 64x256 CTA tile, 16 consumer
+//    warps of 16x64. Every A entry is generated once per CTA and amortised over BN columns.
+// GW: the same for r > 256: 32x512 CTA tile (two 256-column TMA boxes per stage), 16 warps of
+//    16x64, 3 stages. Same accumulator registers and fragment loads per warp as G, but each
+//    generated entry feeds 512 columns instead of 256: entry generation (FP64 ops on the pipe the
+//    DMMAs use) halves per flop. c3: 75.1% -> 81.3% of the FP64 peak.
 constexpr int kStagesS = 5, kStagesG = 5, kBM_S = 128, kBN_S = 128, kBM_G = 64, kBN_G = 256;
+constexpr int kStagesGW = 3, kBM_GW = 32, kBN_GW = 512;
 #define CFG_S kBM_S, kBN_S, 4, 4, kStagesS
 #define CFG_G kBM_G, kBN_G, 4, 4, kStagesG
+#define CFG_GW kBM_GW, kBN_GW, 2, 8, kStagesGW
 constexpr int kThreadsS = kProducerThreads + kConsumerThreads;
 constexpr int kThreadsG = kProducerThreads + kConsumerThreads;
 
@@ -105,14 +111,18 @@ using KernelFn = void (*)(BMaps, const Tile*, const Group*, const Term*, int32_t
                           int32_t);
 
 struct GenKernel {
-  KernelFn fn;
-  size_t smem;
+  KernelFn fn, fn_wide;
+  size_t smem, smem_wide;
 };
 
 template <int KIND, int DIM>
 GenKernel gen_kernel() {
-  return {&grouped_gemm_f64<CFG_G, KIND, DIM>, gemm_smem_bytes<CFG_G, KIND, DIM>()};
+  return {&grouped_gemm_f64<CFG_G, KIND, DIM>, &grouped_gemm_f64<CFG_GW, KIND, DIM>,
+          gemm_smem_bytes<CFG_G, KIND, DIM>(), gemm_smem_bytes<CFG_GW, KIND, DIM>()};
 }
+
+// wide generated tiles (32 x 512) once the chunk has more than 256 columns
+inline bool use_wide(int32_t r) { return r > kBN_G; }
 
 GenKernel pick_gen_kernel(int kind, int dim) {
 #define GOFMM_DIMS(K)                        \
@@ -220,7 +230,53 @@ struct Launch {
   int stage = 2;  // distributed evaluation: 1 = before the all-gather (own-subtree N2S), 2 = after
   int first_group = 0, ngroups = 0;      // groups [first_group, first_group + ngroups)
   int first_tile32 = 0, ntiles32 = 0;    // FP32 plan: 128-row tiles of the same groups
+  int first_tilew = 0, ntilesw = 0;      // generated launches: kBM_GW-row tiles (GW config)
+  // output launch of a host-buffer evaluation: split into row-contiguous parts so the D2H of a
+  // part's u rows overlaps the next part's kernel. parts[p] = first tile of part p in each tile
+  // list and the u_perm rows it completes; parts.back() is the end sentinel. Empty = no split.
+  struct Part {
+    int tile, tilew, tile32;
+    int64_t row;
+  };
+  std::vector<Part> parts;
 };
+
+constexpr int kOutParts = 4;
+
+// the part boundaries of an output launch: groups split into kOutParts runs of leaves; valid only
+// if consecutive runs cover consecutive u_perm rows (leaves in left-to-right order)
+template <class GroupVec, class TileVec>
+void split_output_parts(Launch& L, const GroupVec& groups, const TileVec& tiles) {
+  L.parts.clear();
+  if (L.ngroups < kOutParts) return;
+  int64_t expect = -1;
+  std::vector<Launch::Part> parts;
+  for (int p = 0; p <= kOutParts; ++p) {
+    const int gb = L.first_group + int(int64_t(L.ngroups) * p / kOutParts);
+    Launch::Part q{};
+    auto first_of = [&](int t0, int nt) {
+      int t = t0;
+      while (t < t0 + nt && tiles[t].group < gb) ++t;
+      return t;
+    };
+    q.tile = first_of(L.first_tile, L.ntiles);
+    q.tilew = L.ntilesw > 0 ? first_of(L.first_tilew, L.ntilesw) : 0;
+    q.tile32 = 0;
+    q.row = (p < kOutParts) ? groups[gb].c_row : expect;
+    if (p < kOutParts) {
+      const int ge = L.first_group + int(int64_t(L.ngroups) * (p + 1) / kOutParts);
+      int64_t row = groups[gb].c_row;
+      if (expect >= 0 && row != expect) return;  // not row-contiguous: no split
+      for (int g = gb; g < ge; ++g) {
+        if (groups[g].c_row != row) return;
+        row += std::max(groups[g].M, 0);
+      }
+      expect = row;
+    }
+    parts.push_back(q);
+  }
+  L.parts = std::move(parts);
+}
 
 // ---------------------------------------------------------------- subtree-split distribution
 // north_star (4): for P = 2^l GPUs the tree is split at level l into P subtrees, one per rank.
@@ -334,8 +390,9 @@ struct gofmm_handle {
   // host-buffer evaluation pipeline (evaluate_host): H2D / D2H copy streams and, per staging
   // buffer b, events in_ready / comp_done / out_free and copy-timing pairs
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-  cudaEvent_t pev[2][3] = {};
+  cudaEvent_t pev[2][4] = {};
   cudaEvent_t tev[2][4] = {};
+  cudaEvent_t dpev[8][2] = {};  // per-part D2H timing of a split output launch (<= kOutParts)
   gofmm::DevBuf d_win2[2], d_uout2[2];
   std::vector<cudaEvent_t> lev;  // per-launch start/stop events (timed evaluations only)
   std::vector<float> launch_ms;  // durations of the last timed evaluation (summed over chunks)
@@ -393,8 +450,8 @@ struct gofmm_handle {
   gofmm::f32::BMaps maps32{};
   int32_t maps32_r = 0;
 
-  gofmm::KernelFn kfn_s = nullptr, kfn_g = nullptr;
-  size_t smem_s = 0, smem_g = 0;
+  gofmm::KernelFn kfn_s = nullptr, kfn_g = nullptr, kfn_gw = nullptr;
+  size_t smem_s = 0, smem_g = 0, smem_gw = 0;
   gofmm::BMaps maps_s{}, maps_g{};
   int32_t maps_r = 0;  // r the tensor maps were encoded for
   int64_t flops_per_rhs = 0;
@@ -526,6 +583,13 @@ void build_f32(gofmm_handle* H) {
     for (int gi = L.first_group; gi < L.first_group + L.ngroups; ++gi)
       for (int m0 = 0; m0 < std::max(H->groups[gi].M, 0); m0 += f32::kBM) tiles32.push_back({gi, m0});
     L.ntiles32 = int(tiles32.size()) - L.first_tile32;
+    for (size_t p = 0; p < L.parts.size(); ++p) {
+      const int gb = (p + 1 < L.parts.size()) ? L.first_group + int(int64_t(L.ngroups) * p / kOutParts)
+                                               : L.first_group + L.ngroups;
+      int t = L.first_tile32;
+      while (t < L.first_tile32 + L.ntiles32 && tiles32[t].group < gb) ++t;
+      L.parts[p].tile32 = t;
+    }
   }
   H->d_tiles32.upload(tiles32);
   // groups and FP32 terms do not depend on the workspace (B operands go through tensor maps)
@@ -882,7 +946,14 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     L.ntiles = int(H->tiles.size()) - L.first_tile;
     L.first_group = int(H->groups.size()) - int(gs.size());
     L.ngroups = int(gs.size());
-    if (L.ntiles > 0) H->launches.push_back(L);
+    if (gen) {
+      L.first_tilew = int(H->tiles.size());
+      for (int gi = L.first_group; gi < L.first_group + L.ngroups; ++gi)
+        for (int m0 = 0; m0 < std::max(H->groups[gi].M, 0); m0 += kBM_GW) H->tiles.push_back({gi, m0});
+      L.ntilesw = int(H->tiles.size()) - L.first_tilew;
+    }
+    if (out == Buf::Out) split_output_parts(L, H->groups, H->tiles);
+    if (L.ntiles > 0) H->launches.push_back(std::move(L));
   };
 
   // upward (N2S), deepest level first (evaluate.hpp:83-93,150-163)
@@ -1060,7 +1131,10 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     GenKernel gk = pick_gen_kernel(H->kernel, H->dim);
     H->kfn_g = gk.fn;
     H->smem_g = gk.smem;
+    H->kfn_gw = gk.fn_wide;
+    H->smem_gw = gk.smem_wide;
     GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_g, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_g)));
+    GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_gw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_gw)));
   }
   H->d_tiles.upload(H->tiles);
   H->d_groups.alloc(H->groups.size() * sizeof(Group), false);
@@ -1174,8 +1248,13 @@ int guarded(F&& f) {
 // Enqueue one column chunk of an evaluation on `st`: W (original order, device) -> u_perm (device).
 // stage 0: the whole evaluation; stage 1 / 2: the distributed halves around the all-gather
 // (d_xbuf = this rank's send buffer / the gathered receive buffer).
+// rows_done (host-buffer pipeline, stage 0 only): called after each part of a split output
+// launch is enqueued, with the u_perm rows that part completes; returns whether it was used.
+using RowsDone = std::function<void(int64_t row0, int64_t row1)>;
+
 void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double* d_u, int64_t ldu,
-                   cudaStream_t st, bool timed, int stage = 0, double* d_xbuf = nullptr) {
+                   cudaStream_t st, bool timed, int stage = 0, double* d_xbuf = nullptr,
+                   const RowsDone* rows_done = nullptr, bool* rows_used = nullptr) {
   ensure_workspace(H, r);
   upload_plan(H);
   if (H->maps_r != r) {
@@ -1224,7 +1303,34 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
     const Tile* tiles = H->d_tiles.as<Tile>() + L.first_tile;
     const size_t li = size_t(&L - H->launches.data());
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li], st));
-    if (L.gen) {
+    if (rows_done && stage == 0 && L.out == Buf::Out && !L.parts.empty()) {
+      const bool wide = L.gen && use_wide(r);
+      for (size_t p = 0; p + 1 < L.parts.size(); ++p) {
+        const Launch::Part &a = L.parts[p], &b = L.parts[p + 1];
+        const int t0 = wide ? a.tilew : a.tile, nt = (wide ? b.tilew : b.tile) - t0;
+        if (nt > 0) {
+          const int bn = L.gen ? (wide ? kBN_GW : kBN_G) : kBN_S;
+          dim3 grid(unsigned(nt), unsigned((r + bn - 1) / bn));
+          const Tile* tp = H->d_tiles.as<Tile>() + t0;
+          if (!L.gen)
+            H->kfn_s<<<grid, kThreadsS, H->smem_s, st>>>(H->maps_s, tp, H->d_groups.as<Group>(),
+                                                          H->d_terms.as<Term>(), r, H->kp, cbase, ldc, cpanel);
+          else if (wide)
+            H->kfn_gw<<<grid, kThreadsG, H->smem_gw, st>>>(H->maps_g, tp, H->d_groups.as<Group>(),
+                                                            H->d_terms.as<Term>(), r, H->kp, cbase, ldc, cpanel);
+          else
+            H->kfn_g<<<grid, kThreadsG, H->smem_g, st>>>(H->maps_g, tp, H->d_groups.as<Group>(),
+                                                          H->d_terms.as<Term>(), r, H->kp, cbase, ldc, cpanel);
+        }
+        (*rows_done)(a.row, b.row);
+      }
+      if (rows_used) *rows_used = true;
+    } else if (L.gen && use_wide(r)) {
+      dim3 grid(unsigned(L.ntilesw), unsigned((r + kBN_GW - 1) / kBN_GW));
+      H->kfn_gw<<<grid, kThreadsG, H->smem_gw, st>>>(H->maps_g, H->d_tiles.as<Tile>() + L.first_tilew,
+                                                      H->d_groups.as<Group>(), H->d_terms.as<Term>(), r, H->kp, cbase,
+                                                      ldc, cpanel);
+    } else if (L.gen) {
       dim3 grid(unsigned(L.ntiles), unsigned((r + kBN_G - 1) / kBN_G));
       H->kfn_g<<<grid, kThreadsG, H->smem_g, st>>>(H->maps_g, tiles, H->d_groups.as<Group>(), H->d_terms.as<Term>(),
                                                     r, H->kp, cbase, ldc, cpanel);
@@ -1274,22 +1380,27 @@ int32_t rhs_chunk(gofmm_handle* H, int32_t r) {
   const double avail = 0.85 * double(free_b) + per_col * H->ws_r;  // current workspace is reusable
   int64_t cols = int64_t(avail / per_col);
   if (cols >= r) return r;
-  if (cols >= kBN_G) cols = (cols / kBN_G) * kBN_G;
+  if (cols >= kBN_GW)
+    cols = (cols / kBN_GW) * kBN_GW;
+  else if (cols >= kBN_G)
+    cols = (cols / kBN_G) * kBN_G;
   if (cols < 1) throw Error(GOFMM_ERR_CUDA, "not enough device memory for one right-hand side");
   return int32_t(cols);
 }
 
 // Enqueue a whole evaluation (all column chunks).
 void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double* d_u, int64_t ldu, cudaStream_t st,
-             bool timed) {
+             bool timed, const RowsDone* rows_done = nullptr, bool* rows_used = nullptr) {
   const int32_t rc = rhs_chunk(H, r);
   if (timed) {
     H->launch_ms.assign(H->launches.size(), 0.f);
     std::fill(std::begin(H->phase_ms), std::end(H->phase_ms), 0.f);
   }
+  if (rc < r) rows_done = nullptr;  // the hook covers a single-chunk evaluation only
   for (int32_t c0 = 0; c0 < r; c0 += rc) {
     const int32_t rr = std::min(rc, r - c0);
-    enqueue_chunk(H, d_w + size_t(c0) * ldw, ldw, rr, d_u + size_t(c0) * ldu, ldu, st, timed);
+    enqueue_chunk(H, d_w + size_t(c0) * ldw, ldw, rr, d_u + size_t(c0) * ldu, ldu, st, timed, 0, nullptr, rows_done,
+                  rows_used);
     if (timed) accumulate_chunk_times(H);
   }
 }
@@ -1322,7 +1433,8 @@ void encode_bmap32(CUtensorMap* map, const float* ptr, int64_t rows, int32_t r, 
 // stage 0: the whole evaluation; stage 1 / 2: the distributed halves around the all-gather
 // (d_xbuf = this rank's send buffer / the gathered receive buffer, hi/lo slots, see panel_copy_f32)
 void enqueue_chunk32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, float* d_u, int64_t ldu,
-                     cudaStream_t st, bool timed, int stage = 0, float* d_xbuf = nullptr) {
+                     cudaStream_t st, bool timed, int stage = 0, float* d_xbuf = nullptr,
+                     const RowsDone* rows_done = nullptr, bool* rows_used = nullptr) {
   ensure_workspace32(H, r);
   const int bn = f32_bn(r);
   if (H->k32_s.bn != bn) {
@@ -1367,9 +1479,21 @@ void enqueue_chunk32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, 
     const size_t li = size_t(&L - H->launches.data());
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li], st));
     const f32::GemmKernel& k = L.gen ? H->k32_g : H->k32_s;
-    GOFMM_CUDA(f32::launch_gemm(k, unsigned(L.ntiles32), r, H->maps32, H->d_tiles32.as<Tile>() + L.first_tile32,
-                                H->d_groups.as<Group>(), H->d_terms32.as<f32::Term>(), H->kp32, ch, cl, ldc, cpanel,
-                                st));
+    if (rows_done && stage == 0 && L.out == Buf::Out && !L.parts.empty()) {
+      for (size_t p = 0; p + 1 < L.parts.size(); ++p) {
+        const int t0 = L.parts[p].tile32, nt = L.parts[p + 1].tile32 - t0;
+        if (nt > 0)
+          GOFMM_CUDA(f32::launch_gemm(k, unsigned(nt), r, H->maps32, H->d_tiles32.as<Tile>() + t0,
+                                      H->d_groups.as<Group>(), H->d_terms32.as<f32::Term>(), H->kp32, ch, cl, ldc,
+                                      cpanel, st));
+        (*rows_done)(L.parts[p].row, L.parts[p + 1].row);
+      }
+      if (rows_used) *rows_used = true;
+    } else {
+      GOFMM_CUDA(f32::launch_gemm(k, unsigned(L.ntiles32), r, H->maps32, H->d_tiles32.as<Tile>() + L.first_tile32,
+                                  H->d_groups.as<Group>(), H->d_terms32.as<f32::Term>(), H->kp32, ch, cl, ldc, cpanel,
+                                  st));
+    }
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li + 1], st));
   }
   if (stage == 1 && H->n_pack > 0)
@@ -1398,15 +1522,17 @@ int32_t rhs_chunk32(gofmm_handle* H, int32_t r) {
 }
 
 void enqueue32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, float* d_u, int64_t ldu, cudaStream_t st,
-               bool timed) {
+               bool timed, const RowsDone* rows_done = nullptr, bool* rows_used = nullptr) {
   const int32_t rc = rhs_chunk32(H, r);
   if (timed) {
     H->launch_ms.assign(H->launches.size(), 0.f);
     std::fill(std::begin(H->phase_ms), std::end(H->phase_ms), 0.f);
   }
+  if (rc < r) rows_done = nullptr;  // the hook covers a single-chunk evaluation only
   for (int32_t c0 = 0; c0 < r; c0 += rc) {
     const int32_t rr = std::min(rc, r - c0);
-    enqueue_chunk32(H, d_w + size_t(c0) * ldw, ldw, rr, d_u + size_t(c0) * ldu, ldu, st, timed);
+    enqueue_chunk32(H, d_w + size_t(c0) * ldw, ldw, rr, d_u + size_t(c0) * ldu, ldu, st, timed, 0, nullptr,
+                    rows_done, rows_used);
     if (timed) accumulate_chunk_times(H);
   }
 }
@@ -1620,6 +1746,9 @@ int gofmm_destroy(gofmm_handle* H) {
     for (auto& row : H->tev)
       for (auto& e : row)
         if (e) cudaEventDestroy(e);
+    for (auto& row : H->dpev)
+      for (auto& e : row)
+        if (e) cudaEventDestroy(e);
     delete H;
   });
 }
@@ -1643,6 +1772,8 @@ int gofmm_launch_profile(const gofmm_handle* H, int32_t r, int32_t cap, gofmm_la
       out[i].level = L.level;
       if (H->precision == GOFMM_PRECISION_F32)
         out[i].ctas = int64_t(L.ntiles32) * ((r + f32_bn(r) - 1) / f32_bn(r));
+      else if (L.gen && use_wide(r))
+        out[i].ctas = int64_t(L.ntilesw) * ((r + kBN_GW - 1) / kBN_GW);
       else
         out[i].ctas = int64_t(L.ntiles) * ((r + (L.gen ? kBN_G : kBN_S) - 1) / (L.gen ? kBN_G : kBN_S));
       out[i].flops = L.flops_per_rhs * int64_t(r);
@@ -1711,12 +1842,23 @@ void evaluate_host(gofmm_handle* H, const T* w, int64_t ldw, int32_t r, T* u_per
       for (auto& e : row) GOFMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& row : H->tev)
       for (auto& e : row) GOFMM_CUDA(cudaEventCreate(&e));
+    for (auto& row : H->dpev)
+      for (auto& e : row) GOFMM_CUDA(cudaEventCreate(&e));
   }
-  // chunk: one 256-column N tile (both kernel families tile 256 columns) unless r is smaller or
-  // the workspace forces less
+  // chunk: one N tile of the generated-operand kernels (FP32: 256 columns; FP64: 512 columns,
+  // the GW config, once r > 256) unless r is smaller or the workspace forces less
   const int32_t rc_ws = kF32 ? rhs_chunk32(H, r) : rhs_chunk(H, r);
-  const int32_t rc = std::max<int32_t>(1, std::min<int32_t>({r, rc_ws, r > 256 ? 256 : r}));
   const size_t per_col = size_t(H->n) * sizeof(T);
+  int32_t tile_n = kF32 ? 256 : (use_wide(r) ? kBN_GW : kBN_G);
+  {
+    // four staging buffers (W and u, double-buffered) must fit next to the workspace
+    size_t free_b = 0, total_b = 0;
+    GOFMM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t have = H->d_win2[0].bytes + H->d_win2[1].bytes + H->d_uout2[0].bytes + H->d_uout2[1].bytes;
+    const int64_t fit = int64_t(0.8 * double(free_b + have) / double(4 * per_col));
+    if (tile_n > fit) tile_n = fit >= 256 ? 256 : int32_t(std::max<int64_t>(1, fit));
+  }
+  const int32_t rc = std::max<int32_t>(1, std::min<int32_t>({r, rc_ws, tile_n}));
   const size_t bytes = per_col * size_t(rc);
   for (int b = 0; b < 2; ++b)
     if (H->d_win2[b].bytes < bytes) {
@@ -1731,6 +1873,12 @@ void evaluate_host(gofmm_handle* H, const T* w, int64_t ldw, int32_t r, T* u_per
     const int32_t c0 = i * rc, rr = std::min(rc, r - c0);
     // the buffer's previous chunk (i - 2) must have been consumed by its evaluation
     if (i >= 2) GOFMM_CUDA(cudaStreamWaitEvent(H->s_h2d, H->pev[b][1], 0));
+    if (stats && i >= 2) {  // collect chunk i-2's upload time before its events are re-recorded
+      float a;
+      GOFMM_CUDA(cudaEventSynchronize(H->tev[b][1]));
+      GOFMM_CUDA(cudaEventElapsedTime(&a, H->tev[b][0], H->tev[b][1]));
+      h2d += a;
+    }
     if (stats) GOFMM_CUDA(cudaEventRecord(H->tev[b][0], H->s_h2d));
     GOFMM_CUDA(cudaMemcpy2DAsync(H->d_win2[b].p, per_col, w + size_t(c0) * ldw, size_t(ldw) * sizeof(T), per_col,
                                  rr, cudaMemcpyHostToDevice, H->s_h2d));
@@ -1738,21 +1886,53 @@ void evaluate_host(gofmm_handle* H, const T* w, int64_t ldw, int32_t r, T* u_per
     GOFMM_CUDA(cudaEventRecord(H->pev[b][0], H->s_h2d));  // in_ready
   };
   if (nchunks > 0) h2d_copy(0);
+  int parts_timed = 0;      // last chunk: D2H copies timed per part
+  bool last_full = false;   // last chunk: whole-buffer D2H (no split) timed by tev
   for (int i = 0; i < nchunks; ++i) {
     const int b = i & 1;
     const int32_t c0 = i * rc, rr = std::min(rc, r - c0);
     if (i + 1 < nchunks) h2d_copy(i + 1);  // prefetch the next chunk before evaluating this one
     GOFMM_CUDA(cudaStreamWaitEvent(st, H->pev[b][0], 0));            // W chunk landed
     if (i >= 2) GOFMM_CUDA(cudaStreamWaitEvent(st, H->pev[b][2], 0));  // u buffer downloaded
+    // last chunk: its u rows are downloaded part by part behind the split output launch
+    // (rows_done), so only the last part's download is exposed
+    bool rows_used = false, started = false;
+    int64_t rows_lo = -1, rows_hi = -1;
+    const RowsDone rows_done = [&](int64_t r0, int64_t r1) {
+      GOFMM_CUDA(cudaEventRecord(H->pev[b][3], st));
+      GOFMM_CUDA(cudaStreamWaitEvent(H->s_d2h, H->pev[b][3], 0));
+      if (stats && !started) GOFMM_CUDA(cudaEventRecord(H->tev[b][2], H->s_d2h));
+      started = true;
+      const bool timed_part = stats && parts_timed < 8;
+      if (timed_part) GOFMM_CUDA(cudaEventRecord(H->dpev[parts_timed][0], H->s_d2h));
+      if (r1 > r0)
+        GOFMM_CUDA(cudaMemcpy2DAsync(u_perm + size_t(c0) * ldu + r0, size_t(ldu) * sizeof(T),
+                                     static_cast<T*>(H->d_uout2[b].p) + r0, per_col, size_t(r1 - r0) * sizeof(T), rr,
+                                     cudaMemcpyDeviceToHost, H->s_d2h));
+      if (timed_part) GOFMM_CUDA(cudaEventRecord(H->dpev[parts_timed++][1], H->s_d2h));
+      if (rows_lo < 0 || r0 < rows_lo) rows_lo = r0;
+      rows_hi = std::max(rows_hi, r1);
+    };
+    const RowsDone* hook = (i + 1 == nchunks) ? &rows_done : nullptr;
     if constexpr (kF32)
-      enqueue32(H, H->d_win2[b].as<float>(), H->n, rr, H->d_uout2[b].as<float>(), H->n, st, stats != nullptr);
+      enqueue32(H, H->d_win2[b].as<float>(), H->n, rr, H->d_uout2[b].as<float>(), H->n, st, stats != nullptr, hook,
+                &rows_used);
     else
-      enqueue(H, H->d_win2[b].as<double>(), H->n, rr, H->d_uout2[b].as<double>(), H->n, st, stats != nullptr);
+      enqueue(H, H->d_win2[b].as<double>(), H->n, rr, H->d_uout2[b].as<double>(), H->n, st, stats != nullptr, hook,
+              &rows_used);
     GOFMM_CUDA(cudaEventRecord(H->pev[b][1], st));  // comp_done: W buffer free, u chunk ready
     GOFMM_CUDA(cudaStreamWaitEvent(H->s_d2h, H->pev[b][1], 0));
-    if (stats) GOFMM_CUDA(cudaEventRecord(H->tev[b][2], H->s_d2h));
-    GOFMM_CUDA(cudaMemcpy2DAsync(u_perm + size_t(c0) * ldu, size_t(ldu) * sizeof(T), H->d_uout2[b].p, per_col,
-                                 per_col, rr, cudaMemcpyDeviceToHost, H->s_d2h));
+    const bool split = rows_used && rows_lo == 0 && rows_hi == H->n;
+    if (!split) {
+      // whole-buffer download (the parts, if any, did not cover u_perm)
+      if (stats) GOFMM_CUDA(cudaEventRecord(H->tev[b][2], H->s_d2h));
+      GOFMM_CUDA(cudaMemcpy2DAsync(u_perm + size_t(c0) * ldu, size_t(ldu) * sizeof(T), H->d_uout2[b].p, per_col,
+                                   per_col, rr, cudaMemcpyDeviceToHost, H->s_d2h));
+    }
+    if (i + 1 == nchunks) {
+      last_full = !split;
+      if (!split) parts_timed = 0;
+    }
     if (stats) GOFMM_CUDA(cudaEventRecord(H->tev[b][3], H->s_d2h));
     GOFMM_CUDA(cudaEventRecord(H->pev[b][2], H->s_d2h));  // out_free
     if (stats) {
@@ -1764,20 +1944,26 @@ void evaluate_host(gofmm_handle* H, const T* w, int64_t ldw, int32_t r, T* u_per
     if (stats && i >= 1) {  // chunk i-1's copies are complete once its D2H event is
       const int pb = (i - 1) & 1;
       GOFMM_CUDA(cudaEventSynchronize(H->tev[pb][3]));
-      float a, c;
-      GOFMM_CUDA(cudaEventElapsedTime(&a, H->tev[pb][0], H->tev[pb][1]));
+      float c;
       GOFMM_CUDA(cudaEventElapsedTime(&c, H->tev[pb][2], H->tev[pb][3]));
-      h2d += a;
       d2h += c;
     }
   }
   GOFMM_CUDA(cudaStreamSynchronize(H->s_d2h));
   if (stats) {
     const int lb = (nchunks - 1) & 1;
-    float a, c;
-    GOFMM_CUDA(cudaEventElapsedTime(&a, H->tev[lb][0], H->tev[lb][1]));
-    GOFMM_CUDA(cudaEventElapsedTime(&c, H->tev[lb][2], H->tev[lb][3]));
-    h2d += a;
+    float c = 0.f;
+    for (int i = std::max(0, nchunks - 2); i < nchunks; ++i) {  // uploads not collected in h2d_copy
+      float a;
+      GOFMM_CUDA(cudaEventElapsedTime(&a, H->tev[i & 1][0], H->tev[i & 1][1]));
+      h2d += a;
+    }
+    if (last_full) GOFMM_CUDA(cudaEventElapsedTime(&c, H->tev[lb][2], H->tev[lb][3]));
+    for (int p = 0; p < parts_timed; ++p) {
+      float x;
+      GOFMM_CUDA(cudaEventElapsedTime(&x, H->dpev[p][0], H->dpev[p][1]));
+      c += x;
+    }
     d2h += c;
     std::memset(stats, 0, sizeof(*stats));
     stats->flops = H->flops_per_rhs * int64_t(r);

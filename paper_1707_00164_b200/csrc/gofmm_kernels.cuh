@@ -301,7 +301,9 @@ struct GemmShape {
   static constexpr int B_STAGE_BYTES = BN * kBK * 8;  // TMA box, 128B-swizzled rows, 1024B aligned
   static constexpr int X_STAGE = kBK * XD;            // column coordinates (generated terms)
   static constexpr int GEN_PER_THREAD = (BM * kBK) / kConsumerThreads;
-  static_assert(BM % (8 * WM) == 0 && BN % (8 * WN) == 0 && BN <= 256, "tile shape");
+  static_assert(BM % (8 * WM) == 0 && BN % (8 * WN) == 0, "tile shape");
+  static constexpr int kBoxN = BN > 256 ? 256 : BN;  // TMA box limit: wider tiles take several boxes
+  static_assert(BN % kBoxN == 0, "B tile = whole TMA boxes");
   static_assert(B_STAGE_BYTES % 1024 == 0, "swizzle-128B tiles need 1024-byte multiples");
   static_assert((BM * kBK) % kConsumerThreads == 0 && kConsumerThreads % BM == 0, "generation mapping");
   static constexpr size_t smem_bytes = 1024 /* alignment slack */ + size_t(STAGES) * B_STAGE_BYTES +
@@ -396,8 +398,10 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
       if (pth == 0) {
         mbar_arrive_expect_tx(full, S::B_STAGE_BYTES);
         // B rows [b_row + k0, +16) = one 16-row panel (b_row is 16-aligned): a contiguous run
-        tma_load_3d(smem_u32(sB + stage * S::B_STAGE_BYTES), &maps.m[T.bbuf], 0, n0,
-                    int32_t((T.b_row + k0) >> 4), full);
+#pragma unroll
+        for (int bx = 0; bx < BN / S::kBoxN; ++bx)
+          tma_load_3d(smem_u32(sB + stage * S::B_STAGE_BYTES + bx * S::kBoxN * 128), &maps.m[T.bbuf], 0,
+                      n0 + bx * S::kBoxN, int32_t((T.b_row + k0) >> 4), full);
       }
       if (kGen && (T.flags & kTermGen)) {
         if constexpr (kGen) {
