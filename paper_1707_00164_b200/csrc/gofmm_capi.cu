@@ -101,9 +101,13 @@ struct DevBuf {
 //    DMMAs use) halves per flop. c3: 75.1% -> 81.3% of the FP64 peak.
 constexpr int kStagesS = 5, kStagesG = 5, kBM_S = 128, kBN_S = 128, kBM_G = 64, kBN_G = 256;
 constexpr int kStagesGW = 3, kBM_GW = 32, kBN_GW = 512;
+// GN64 / GN128: the same 64-row tiles for r <= 64 / r <= 128 (config 1: r = 64), so no CTA
+// multiplies zero columns and each k-stage is 4x / 2x shorter along the serial term chain.
 #define CFG_S kBM_S, kBN_S, 4, 4, kStagesS
 #define CFG_G kBM_G, kBN_G, 4, 4, kStagesG
 #define CFG_GW kBM_GW, kBN_GW, 2, 8, kStagesGW
+#define CFG_GN64 kBM_G, 64, 4, 4, kStagesG
+#define CFG_GN128 kBM_G, 128, 4, 4, kStagesG
 constexpr int kThreadsS = kProducerThreads + kConsumerThreads;
 constexpr int kThreadsG = kProducerThreads + kConsumerThreads;
 
@@ -111,14 +115,16 @@ using KernelFn = void (*)(BMaps, const Tile*, const Group*, const Term*, int32_t
                           int32_t);
 
 struct GenKernel {
-  KernelFn fn, fn_wide;
-  size_t smem, smem_wide;
+  KernelFn fn, fn_wide, fn_n64, fn_n128;
+  size_t smem, smem_wide, smem_n64, smem_n128;
 };
 
 template <int KIND, int DIM>
 GenKernel gen_kernel() {
-  return {&grouped_gemm_f64<CFG_G, KIND, DIM>, &grouped_gemm_f64<CFG_GW, KIND, DIM>,
-          gemm_smem_bytes<CFG_G, KIND, DIM>(), gemm_smem_bytes<CFG_GW, KIND, DIM>()};
+  return {&grouped_gemm_f64<CFG_G, KIND, DIM>,           &grouped_gemm_f64<CFG_GW, KIND, DIM>,
+          &grouped_gemm_f64<CFG_GN64, KIND, DIM>,        &grouped_gemm_f64<CFG_GN128, KIND, DIM>,
+          gemm_smem_bytes<CFG_G, KIND, DIM>(),           gemm_smem_bytes<CFG_GW, KIND, DIM>(),
+          gemm_smem_bytes<CFG_GN64, KIND, DIM>(),        gemm_smem_bytes<CFG_GN128, KIND, DIM>()};
 }
 
 // wide generated tiles (32 x 512) once the chunk has more than 256 columns
@@ -450,9 +456,9 @@ struct gofmm_handle {
   gofmm::f32::BMaps maps32{};
   int32_t maps32_r = 0;
 
-  gofmm::KernelFn kfn_s = nullptr, kfn_g = nullptr, kfn_gw = nullptr;
-  size_t smem_s = 0, smem_g = 0, smem_gw = 0;
-  gofmm::BMaps maps_s{}, maps_g{};
+  gofmm::KernelFn kfn_s = nullptr, kfn_g = nullptr, kfn_gw = nullptr, kfn_gn64 = nullptr, kfn_gn128 = nullptr;
+  size_t smem_s = 0, smem_g = 0, smem_gw = 0, smem_gn64 = 0, smem_gn128 = 0;
+  gofmm::BMaps maps_s{}, maps_g{}, maps_n64{};  // B boxes of 128 / 256 / 64 columns
   int32_t maps_r = 0;  // r the tensor maps were encoded for
   int64_t flops_per_rhs = 0;
   int64_t phase_flops_per_rhs[3] = {0, 0, 0};  // upward, downward, output
@@ -1133,6 +1139,12 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     H->smem_g = gk.smem;
     H->kfn_gw = gk.fn_wide;
     H->smem_gw = gk.smem_wide;
+    H->kfn_gn64 = gk.fn_n64;
+    H->smem_gn64 = gk.smem_n64;
+    H->kfn_gn128 = gk.fn_n128;
+    H->smem_gn128 = gk.smem_n128;
+    GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_gn64, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_gn64)));
+    GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_gn128, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_gn128)));
     GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_g, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_g)));
     GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_gw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_gw)));
   }
@@ -1248,6 +1260,37 @@ int guarded(F&& f) {
 // Enqueue one column chunk of an evaluation on `st`: W (original order, device) -> u_perm (device).
 // stage 0: the whole evaluation; stage 1 / 2: the distributed halves around the all-gather
 // (d_xbuf = this rank's send buffer / the gathered receive buffer).
+// B operand tensor maps over the FP64 workspace buffers for this column count
+void encode_maps(gofmm_handle* H, int32_t r) {
+  if (H->maps_r == r) return;
+  {
+    const double* bufs[3] = {H->d_wp.as<double>(), H->d_what.as<double>(), H->d_c.as<double>()};
+    const int64_t rows[3] = {H->ld_wp, H->ld_s, H->ld_s};
+    for (int b = 0; b < 3; ++b) {
+      encode_bmap(&H->maps_s.m[b], bufs[b], rows[b], r, H->ws_r, kBN_S);
+      encode_bmap(&H->maps_g.m[b], bufs[b], rows[b], r, H->ws_r, kBN_G);
+      encode_bmap(&H->maps_n64.m[b], bufs[b], rows[b], r, H->ws_r, 64);
+    }
+    H->maps_r = r;
+  }
+}
+
+// kernel configuration of one launch for a chunk of r columns (tile list, B maps, N tile)
+struct LaunchCfg {
+  KernelFn fn;
+  size_t smem;
+  int bn;
+  const BMaps* maps;
+  bool wide;  // kBM_GW-row tile list
+};
+LaunchCfg pick_launch_cfg(const gofmm_handle* H, const Launch& L, int32_t r) {
+  if (!L.gen) return {H->kfn_s, H->smem_s, kBN_S, &H->maps_s, false};
+  if (use_wide(r)) return {H->kfn_gw, H->smem_gw, kBN_GW, &H->maps_g, true};
+  if (r <= 64) return {H->kfn_gn64, H->smem_gn64, 64, &H->maps_n64, false};
+  if (r <= 128) return {H->kfn_gn128, H->smem_gn128, 128, &H->maps_s, false};
+  return {H->kfn_g, H->smem_g, kBN_G, &H->maps_g, false};
+}
+
 // rows_done (host-buffer pipeline, stage 0 only): called after each part of a split output
 // launch is enqueued, with the u_perm rows that part completes; returns whether it was used.
 using RowsDone = std::function<void(int64_t row0, int64_t row1)>;
@@ -1257,16 +1300,7 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
                    const RowsDone* rows_done = nullptr, bool* rows_used = nullptr) {
   ensure_workspace(H, r);
   upload_plan(H);
-  if (H->maps_r != r) {
-    // B operand tensor maps over the workspace buffers for this column count
-    const double* bufs[3] = {H->d_wp.as<double>(), H->d_what.as<double>(), H->d_c.as<double>()};
-    const int64_t rows[3] = {H->ld_wp, H->ld_s, H->ld_s};
-    for (int b = 0; b < 3; ++b) {
-      encode_bmap(&H->maps_s.m[b], bufs[b], rows[b], r, H->ws_r, kBN_S);
-      encode_bmap(&H->maps_g.m[b], bufs[b], rows[b], r, H->ws_r, kBN_G);
-    }
-    H->maps_r = r;
-  }
+  encode_maps(H, r);
   if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[0], st));
   if (stage == 2 && H->n_unpack > 0) {
     // ghosts: every other rank's exported what / W rows into their places in this workspace
@@ -1300,44 +1334,29 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
       case Buf::C: cbase = H->d_c.as<double>(); ldc = int64_t(H->ws_r) * 16; break;
       default: cbase = d_u; ldc = ldu; cpanel = 0; break;  // u_perm: caller's column-major buffer
     }
-    const Tile* tiles = H->d_tiles.as<Tile>() + L.first_tile;
     const size_t li = size_t(&L - H->launches.data());
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li], st));
+    const LaunchCfg cfg = pick_launch_cfg(H, L, r);
+    auto run = [&](int t0, int nt) {
+      if (nt <= 0) return;
+      dim3 grid(unsigned(nt), unsigned((r + cfg.bn - 1) / cfg.bn));
+      cfg.fn<<<grid, kThreadsG, cfg.smem, st>>>(*cfg.maps, H->d_tiles.as<Tile>() + t0, H->d_groups.as<Group>(),
+                                                 H->d_terms.as<Term>(), r, H->kp, cbase, ldc, cpanel);
+    };
     if (rows_done && stage == 0 && L.out == Buf::Out && !L.parts.empty()) {
-      const bool wide = L.gen && use_wide(r);
       for (size_t p = 0; p + 1 < L.parts.size(); ++p) {
         const Launch::Part &a = L.parts[p], &b = L.parts[p + 1];
-        const int t0 = wide ? a.tilew : a.tile, nt = (wide ? b.tilew : b.tile) - t0;
-        if (nt > 0) {
-          const int bn = L.gen ? (wide ? kBN_GW : kBN_G) : kBN_S;
-          dim3 grid(unsigned(nt), unsigned((r + bn - 1) / bn));
-          const Tile* tp = H->d_tiles.as<Tile>() + t0;
-          if (!L.gen)
-            H->kfn_s<<<grid, kThreadsS, H->smem_s, st>>>(H->maps_s, tp, H->d_groups.as<Group>(),
-                                                          H->d_terms.as<Term>(), r, H->kp, cbase, ldc, cpanel);
-          else if (wide)
-            H->kfn_gw<<<grid, kThreadsG, H->smem_gw, st>>>(H->maps_g, tp, H->d_groups.as<Group>(),
-                                                            H->d_terms.as<Term>(), r, H->kp, cbase, ldc, cpanel);
-          else
-            H->kfn_g<<<grid, kThreadsG, H->smem_g, st>>>(H->maps_g, tp, H->d_groups.as<Group>(),
-                                                          H->d_terms.as<Term>(), r, H->kp, cbase, ldc, cpanel);
-        }
+        if (cfg.wide)
+          run(a.tilew, b.tilew - a.tilew);
+        else
+          run(a.tile, b.tile - a.tile);
         (*rows_done)(a.row, b.row);
       }
       if (rows_used) *rows_used = true;
-    } else if (L.gen && use_wide(r)) {
-      dim3 grid(unsigned(L.ntilesw), unsigned((r + kBN_GW - 1) / kBN_GW));
-      H->kfn_gw<<<grid, kThreadsG, H->smem_gw, st>>>(H->maps_g, H->d_tiles.as<Tile>() + L.first_tilew,
-                                                      H->d_groups.as<Group>(), H->d_terms.as<Term>(), r, H->kp, cbase,
-                                                      ldc, cpanel);
-    } else if (L.gen) {
-      dim3 grid(unsigned(L.ntiles), unsigned((r + kBN_G - 1) / kBN_G));
-      H->kfn_g<<<grid, kThreadsG, H->smem_g, st>>>(H->maps_g, tiles, H->d_groups.as<Group>(), H->d_terms.as<Term>(),
-                                                    r, H->kp, cbase, ldc, cpanel);
+    } else if (cfg.wide) {
+      run(L.first_tilew, L.ntilesw);
     } else {
-      dim3 grid(unsigned(L.ntiles), unsigned((r + kBN_S - 1) / kBN_S));
-      H->kfn_s<<<grid, kThreadsS, H->smem_s, st>>>(H->maps_s, tiles, H->d_groups.as<Group>(), H->d_terms.as<Term>(),
-                                                    r, H->kp, cbase, ldc, cpanel);
+      run(L.first_tile, L.ntiles);
     }
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li + 1], st));
   }
@@ -1772,10 +1791,10 @@ int gofmm_launch_profile(const gofmm_handle* H, int32_t r, int32_t cap, gofmm_la
       out[i].level = L.level;
       if (H->precision == GOFMM_PRECISION_F32)
         out[i].ctas = int64_t(L.ntiles32) * ((r + f32_bn(r) - 1) / f32_bn(r));
-      else if (L.gen && use_wide(r))
-        out[i].ctas = int64_t(L.ntilesw) * ((r + kBN_GW - 1) / kBN_GW);
-      else
-        out[i].ctas = int64_t(L.ntiles) * ((r + (L.gen ? kBN_G : kBN_S) - 1) / (L.gen ? kBN_G : kBN_S));
+      else {
+        const LaunchCfg cfg = pick_launch_cfg(H, L, r);
+        out[i].ctas = int64_t(cfg.wide ? L.ntilesw : L.ntiles) * ((r + cfg.bn - 1) / cfg.bn);
+      }
       out[i].flops = L.flops_per_rhs * int64_t(r);
       out[i].ms = i < int32_t(H->launch_ms.size()) ? H->launch_ms[i] : -1.0;
       out[i].generated = L.gen ? 1 : 0;
@@ -2044,15 +2063,7 @@ int gofmm_exact_rows(gofmm_handle* H, const int32_t* rows, int32_t nrows, const 
     // W_perm for these columns (the permutation of an evaluation)
     ensure_workspace(H, r);
     upload_plan(H);
-    if (H->maps_r != r) {
-      const double* bufs[3] = {H->d_wp.as<double>(), H->d_what.as<double>(), H->d_c.as<double>()};
-      const int64_t rws[3] = {H->ld_wp, H->ld_s, H->ld_s};
-      for (int b = 0; b < 3; ++b) {
-        encode_bmap(&H->maps_s.m[b], bufs[b], rws[b], r, H->ws_r, kBN_S);
-        encode_bmap(&H->maps_g.m[b], bufs[b], rws[b], r, H->ws_r, kBN_G);
-      }
-      H->maps_r = r;
-    }
+    encode_maps(H, r);
     {
       const int cpb = int(std::max<int64_t>(1, std::min<int64_t>(8, (48ll << 20) / (int64_t(H->n) * 8))));
       dim3 grid(unsigned((H->ld_wp + 255) / 256), unsigned((r + cpb - 1) / cpb));
