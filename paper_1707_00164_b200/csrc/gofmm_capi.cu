@@ -28,6 +28,7 @@
 #include <tuple>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -108,6 +109,9 @@ constexpr int kStagesGW = 3, kBM_GW = 32, kBN_GW = 512;
 #define CFG_GW kBM_GW, kBN_GW, 2, 8, kStagesGW
 #define CFG_GN64 kBM_G, 64, 4, 4, kStagesG
 #define CFG_GN128 kBM_G, 128, 4, 4, kStagesG
+// SN64: stored operands for r <= 64 (64x64 tiles: twice the CTAs of S, no idle columns)
+#define CFG_SN64 kBM_G, 64, 4, 4, kStagesS
+constexpr int kBM[3] = {kBM_S, kBM_G, kBM_GW};  // tile-row classes of the FP64 tile lists
 constexpr int kThreadsS = kProducerThreads + kConsumerThreads;
 constexpr int kThreadsG = kProducerThreads + kConsumerThreads;
 
@@ -227,7 +231,8 @@ struct HostGroup {
 };
 
 struct Launch {
-  int first_tile = 0, ntiles = 0;
+  // FP64 tile lists of this launch's groups, one per tile-row class: kBM[c] rows per tile
+  int tfirst[3] = {0, 0, 0}, tn[3] = {0, 0, 0};
   bool gen = false;  // G config (generated operands present)
   Buf out;
   int phase;  // 0 upward, 1 downward, 2 output
@@ -236,12 +241,11 @@ struct Launch {
   int stage = 2;  // distributed evaluation: 1 = before the all-gather (own-subtree N2S), 2 = after
   int first_group = 0, ngroups = 0;      // groups [first_group, first_group + ngroups)
   int first_tile32 = 0, ntiles32 = 0;    // FP32 plan: 128-row tiles of the same groups
-  int first_tilew = 0, ntilesw = 0;      // generated launches: kBM_GW-row tiles (GW config)
   // output launch of a host-buffer evaluation: split into row-contiguous parts so the D2H of a
   // part's u rows overlaps the next part's kernel. parts[p] = first tile of part p in each tile
   // list and the u_perm rows it completes; parts.back() is the end sentinel. Empty = no split.
   struct Part {
-    int tile, tilew, tile32;
+    int tile[3], tile32;
     int64_t row;
   };
   std::vector<Part> parts;
@@ -265,8 +269,7 @@ void split_output_parts(Launch& L, const GroupVec& groups, const TileVec& tiles)
       while (t < t0 + nt && tiles[t].group < gb) ++t;
       return t;
     };
-    q.tile = first_of(L.first_tile, L.ntiles);
-    q.tilew = L.ntilesw > 0 ? first_of(L.first_tilew, L.ntilesw) : 0;
+    for (int c = 0; c < 3; ++c) q.tile[c] = first_of(L.tfirst[c], L.tn[c]);
     q.tile32 = 0;
     q.row = (p < kOutParts) ? groups[gb].c_row : expect;
     if (p < kOutParts) {
@@ -396,6 +399,12 @@ struct gofmm_handle {
   // host-buffer evaluation pipeline (evaluate_host): H2D / D2H copy streams and, per staging
   // buffer b, events in_ready / comp_done / out_free and copy-timing pairs
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  // CUDA graph of a whole single-chunk evaluation (all level launches in one graph),
+  // captured on cap_stream and replayed on the caller's stream while the key matches
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  std::tuple<const void*, int64_t, const void*, int64_t, int32_t, int32_t, int32_t> gkey{};
+  bool graphs = true;  // GOFMM_NO_GRAPH=1 disables replay
   cudaEvent_t pev[2][4] = {};
   cudaEvent_t tev[2][4] = {};
   cudaEvent_t dpev[8][2] = {};  // per-part D2H timing of a split output launch (<= kOutParts)
@@ -456,8 +465,9 @@ struct gofmm_handle {
   gofmm::f32::BMaps maps32{};
   int32_t maps32_r = 0;
 
-  gofmm::KernelFn kfn_s = nullptr, kfn_g = nullptr, kfn_gw = nullptr, kfn_gn64 = nullptr, kfn_gn128 = nullptr;
-  size_t smem_s = 0, smem_g = 0, smem_gw = 0, smem_gn64 = 0, smem_gn128 = 0;
+  gofmm::KernelFn kfn_s = nullptr, kfn_sn64 = nullptr, kfn_g = nullptr, kfn_gw = nullptr, kfn_gn64 = nullptr,
+                  kfn_gn128 = nullptr;
+  size_t smem_s = 0, smem_sn64 = 0, smem_g = 0, smem_gw = 0, smem_gn64 = 0, smem_gn128 = 0;
   gofmm::BMaps maps_s{}, maps_g{}, maps_n64{};  // B boxes of 128 / 256 / 64 columns
   int32_t maps_r = 0;  // r the tensor maps were encoded for
   int64_t flops_per_rhs = 0;
@@ -656,6 +666,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     H->max_chunk = o->max_rhs_chunk;
     H->precision = o->precision;
   }
+  if (const char* e = std::getenv("GOFMM_NO_GRAPH")) H->graphs = !(e[0] == '1');
   auto cp = [&](std::vector<int32_t>& v, const int32_t* p, int64_t k) { v.assign(p, p + k); };
   cp(H->parent, d->parent, nn);
   cp(H->left, d->left, nn);
@@ -936,30 +947,23 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   int64_t flops_mark = 0;
   auto push_launch = [&](std::vector<HostGroup>& gs, bool gen, Buf out, int phase, int level) {
     Launch L;
-    L.first_tile = int(H->tiles.size());
     L.gen = gen;
     L.out = out;
     L.phase = phase;
     L.level = level;
     L.flops_per_rhs = flops - flops_mark;
     flops_mark = flops;
-    const int BM = gen ? kBM_G : kBM_S;
-    for (auto& g : gs) {
-      const int gid = int(H->groups.size());
-      for (int m0 = 0; m0 < std::max(g.M, 0); m0 += BM) H->tiles.push_back({gid, m0});
-      H->groups.push_back(std::move(g));
-    }
-    L.ntiles = int(H->tiles.size()) - L.first_tile;
-    L.first_group = int(H->groups.size()) - int(gs.size());
+    L.first_group = int(H->groups.size());
     L.ngroups = int(gs.size());
-    if (gen) {
-      L.first_tilew = int(H->tiles.size());
+    for (auto& g : gs) H->groups.push_back(std::move(g));
+    for (int c = 0; c < 3; ++c) {
+      L.tfirst[c] = int(H->tiles.size());
       for (int gi = L.first_group; gi < L.first_group + L.ngroups; ++gi)
-        for (int m0 = 0; m0 < std::max(H->groups[gi].M, 0); m0 += kBM_GW) H->tiles.push_back({gi, m0});
-      L.ntilesw = int(H->tiles.size()) - L.first_tilew;
+        for (int m0 = 0; m0 < std::max(H->groups[gi].M, 0); m0 += kBM[c]) H->tiles.push_back({gi, m0});
+      L.tn[c] = int(H->tiles.size()) - L.tfirst[c];
     }
     if (out == Buf::Out) split_output_parts(L, H->groups, H->tiles);
-    if (L.ntiles > 0) H->launches.push_back(std::move(L));
+    if (L.tn[0] > 0) H->launches.push_back(std::move(L));
   };
 
   // upward (N2S), deepest level first (evaluate.hpp:83-93,150-163)
@@ -1133,6 +1137,9 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   H->kfn_s = &grouped_gemm_f64<CFG_S, kKindNone, 1>;
   H->smem_s = gemm_smem_bytes<CFG_S, kKindNone, 1>();
   GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_s)));
+  H->kfn_sn64 = &grouped_gemm_f64<CFG_SN64, kKindNone, 1>;
+  H->smem_sn64 = gemm_smem_bytes<CFG_SN64, kKindNone, 1>();
+  GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_sn64, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_sn64)));
   if (!stored && (gen_near || gen_far)) {
     GenKernel gk = pick_gen_kernel(H->kernel, H->dim);
     H->kfn_g = gk.fn;
@@ -1281,14 +1288,17 @@ struct LaunchCfg {
   size_t smem;
   int bn;
   const BMaps* maps;
-  bool wide;  // kBM_GW-row tile list
+  int bm_class;  // tile list: kBM[bm_class] rows per tile
 };
 LaunchCfg pick_launch_cfg(const gofmm_handle* H, const Launch& L, int32_t r) {
-  if (!L.gen) return {H->kfn_s, H->smem_s, kBN_S, &H->maps_s, false};
-  if (use_wide(r)) return {H->kfn_gw, H->smem_gw, kBN_GW, &H->maps_g, true};
-  if (r <= 64) return {H->kfn_gn64, H->smem_gn64, 64, &H->maps_n64, false};
-  if (r <= 128) return {H->kfn_gn128, H->smem_gn128, 128, &H->maps_s, false};
-  return {H->kfn_g, H->smem_g, kBN_G, &H->maps_g, false};
+  if (!L.gen) {
+    if (r <= 64) return {H->kfn_sn64, H->smem_sn64, 64, &H->maps_n64, 1};
+    return {H->kfn_s, H->smem_s, kBN_S, &H->maps_s, 0};
+  }
+  if (use_wide(r)) return {H->kfn_gw, H->smem_gw, kBN_GW, &H->maps_g, 2};
+  if (r <= 64) return {H->kfn_gn64, H->smem_gn64, 64, &H->maps_n64, 1};
+  if (r <= 128) return {H->kfn_gn128, H->smem_gn128, 128, &H->maps_s, 1};
+  return {H->kfn_g, H->smem_g, kBN_G, &H->maps_g, 1};
 }
 
 // rows_done (host-buffer pipeline, stage 0 only): called after each part of a split output
@@ -1346,17 +1356,12 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
     if (rows_done && stage == 0 && L.out == Buf::Out && !L.parts.empty()) {
       for (size_t p = 0; p + 1 < L.parts.size(); ++p) {
         const Launch::Part &a = L.parts[p], &b = L.parts[p + 1];
-        if (cfg.wide)
-          run(a.tilew, b.tilew - a.tilew);
-        else
-          run(a.tile, b.tile - a.tile);
+        run(a.tile[cfg.bm_class], b.tile[cfg.bm_class] - a.tile[cfg.bm_class]);
         (*rows_done)(a.row, b.row);
       }
       if (rows_used) *rows_used = true;
-    } else if (cfg.wide) {
-      run(L.first_tilew, L.ntilesw);
     } else {
-      run(L.first_tile, L.ntiles);
+      run(L.tfirst[cfg.bm_class], L.tn[cfg.bm_class]);
     }
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li + 1], st));
   }
@@ -1407,10 +1412,47 @@ int32_t rhs_chunk(gofmm_handle* H, int32_t r) {
   return int32_t(cols);
 }
 
+// Replay a captured graph of `body` (which enqueues one whole evaluation on the stream it is
+// given) on `st`; the capture is redone whenever the key (buffers, r, workspace) changes.
+template <class Body>
+void graph_replay(gofmm_handle* H, const decltype(gofmm_handle::gkey)& key, cudaStream_t st, Body&& body) {
+  if (!(H->gexec && H->gkey == key)) {
+    if (H->gexec) {
+      GOFMM_CUDA(cudaGraphExecDestroy(H->gexec));
+      H->gexec = nullptr;
+    }
+    if (!H->cap_stream) GOFMM_CUDA(cudaStreamCreateWithFlags(&H->cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    GOFMM_CUDA(cudaStreamBeginCapture(H->cap_stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      body(H->cap_stream);
+    } catch (...) {
+      cudaStreamEndCapture(H->cap_stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    GOFMM_CUDA(cudaStreamEndCapture(H->cap_stream, &g));
+    const cudaError_t e = cudaGraphInstantiate(&H->gexec, g, 0);
+    cudaGraphDestroy(g);
+    GOFMM_CUDA(e);
+    H->gkey = key;
+  }
+  GOFMM_CUDA(cudaGraphLaunch(H->gexec, st));
+}
+
 // Enqueue a whole evaluation (all column chunks).
 void enqueue(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double* d_u, int64_t ldu, cudaStream_t st,
              bool timed, const RowsDone* rows_done = nullptr, bool* rows_used = nullptr) {
   const int32_t rc = rhs_chunk(H, r);
+  if (H->graphs && !timed && !rows_done && rc >= r) {
+    // everything that allocates or copies synchronously happens before the capture
+    ensure_workspace(H, r);
+    upload_plan(H);
+    encode_maps(H, r);
+    graph_replay(H, {d_w, ldw, d_u, ldu, r, H->ws_r, 64}, st,
+                 [&](cudaStream_t cs) { enqueue_chunk(H, d_w, ldw, r, d_u, ldu, cs, false); });
+    return;
+  }
   if (timed) {
     H->launch_ms.assign(H->launches.size(), 0.f);
     std::fill(std::begin(H->phase_ms), std::end(H->phase_ms), 0.f);
@@ -1449,12 +1491,8 @@ void encode_bmap32(CUtensorMap* map, const float* ptr, int64_t rows, int32_t r, 
   if (rc != CUDA_SUCCESS) throw Error(GOFMM_ERR_CUDA, "cuTensorMapEncodeTiled (fp32) failed: " + std::to_string(int(rc)));
 }
 
-// stage 0: the whole evaluation; stage 1 / 2: the distributed halves around the all-gather
-// (d_xbuf = this rank's send buffer / the gathered receive buffer, hi/lo slots, see panel_copy_f32)
-void enqueue_chunk32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, float* d_u, int64_t ldu,
-                     cudaStream_t st, bool timed, int stage = 0, float* d_xbuf = nullptr,
-                     const RowsDone* rows_done = nullptr, bool* rows_used = nullptr) {
-  ensure_workspace32(H, r);
+// FP32 kernels for this column count (N tile) and the B tensor maps over the workspace
+void prepare32(gofmm_handle* H, int32_t r) {
   const int bn = f32_bn(r);
   if (H->k32_s.bn != bn) {
     H->k32_s = f32::pick_gemm(kKindNone, 1, bn);
@@ -1471,6 +1509,15 @@ void enqueue_chunk32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, 
       for (int p = 0; p < 2; ++p) encode_bmap32(&H->maps32.m[b][p], bufs[b][p], rows[b], r, H->ws32_r, bn);
     H->maps32_r = r;
   }
+}
+
+// stage 0: the whole evaluation; stage 1 / 2: the distributed halves around the all-gather
+// (d_xbuf = this rank's send buffer / the gathered receive buffer, hi/lo slots, see panel_copy_f32)
+void enqueue_chunk32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, float* d_u, int64_t ldu,
+                     cudaStream_t st, bool timed, int stage = 0, float* d_xbuf = nullptr,
+                     const RowsDone* rows_done = nullptr, bool* rows_used = nullptr) {
+  ensure_workspace32(H, r);
+  prepare32(H, r);
   const int64_t pstride = int64_t(H->ws32_r) * 16;
   if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[0], st));
   if (stage == 2 && H->n_unpack > 0)  // ghosts: other ranks' exported what / W rows
@@ -1543,6 +1590,13 @@ int32_t rhs_chunk32(gofmm_handle* H, int32_t r) {
 void enqueue32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, float* d_u, int64_t ldu, cudaStream_t st,
                bool timed, const RowsDone* rows_done = nullptr, bool* rows_used = nullptr) {
   const int32_t rc = rhs_chunk32(H, r);
+  if (H->graphs && !timed && !rows_done && rc >= r) {
+    ensure_workspace32(H, r);
+    prepare32(H, r);
+    graph_replay(H, {d_w, ldw, d_u, ldu, r, H->ws32_r, 32}, st,
+                 [&](cudaStream_t cs) { enqueue_chunk32(H, d_w, ldw, r, d_u, ldu, cs, false); });
+    return;
+  }
   if (timed) {
     H->launch_ms.assign(H->launches.size(), 0.f);
     std::fill(std::begin(H->phase_ms), std::end(H->phase_ms), 0.f);
@@ -1768,6 +1822,8 @@ int gofmm_destroy(gofmm_handle* H) {
     for (auto& row : H->dpev)
       for (auto& e : row)
         if (e) cudaEventDestroy(e);
+    if (H->gexec) cudaGraphExecDestroy(H->gexec);
+    if (H->cap_stream) cudaStreamDestroy(H->cap_stream);
     delete H;
   });
 }
@@ -1793,7 +1849,7 @@ int gofmm_launch_profile(const gofmm_handle* H, int32_t r, int32_t cap, gofmm_la
         out[i].ctas = int64_t(L.ntiles32) * ((r + f32_bn(r) - 1) / f32_bn(r));
       else {
         const LaunchCfg cfg = pick_launch_cfg(H, L, r);
-        out[i].ctas = int64_t(cfg.wide ? L.ntilesw : L.ntiles) * ((r + cfg.bn - 1) / cfg.bn);
+        out[i].ctas = int64_t(L.tn[cfg.bm_class]) * ((r + cfg.bn - 1) / cfg.bn);
       }
       out[i].flops = L.flops_per_rhs * int64_t(r);
       out[i].ms = i < int32_t(H->launch_ms.size()) ? H->launch_ms[i] : -1.0;

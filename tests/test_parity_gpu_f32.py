@@ -157,6 +157,33 @@ def test_f32_device_api(gpu, oracle):
         assert np.array_equal(uo.cpu().numpy(), ev.unpermute(uh))
 
 
+def test_f32_graph_replay_recapture(gpu, oracle, monkeypatch):
+    """FP32 device evaluations through the captured CUDA graph (replays and re-captures on new
+    buffers / r) are bitwise equal to the same evaluations with graphs disabled."""
+    import torch
+
+    pc = oracle.points_gaussian(2000, 3, 4)
+    h = oracle.compress_kernel(oracle.GAUSSIAN, pc, 1.0, m=64, s=48, budget=0.05, seed=4)
+    tree = to_tree(h.export())
+    ws = [oracle.rng_gauss(2000, r, 7 + r).astype(np.float32) for r in (5, 5, 70, 300)]
+    outs = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("GOFMM_NO_GRAPH", flag)
+        with gpu.Evaluator(tree, precision="fp32") as ev:
+            res = []
+            for k in (0, 1, 0, 2, 3, 2):
+                wd = torch.from_numpy(np.ascontiguousarray(ws[k].T)).cuda().t()
+                ud, _ = ev.evaluate_torch(wd)
+                ud2, _ = ev.evaluate_torch(wd, out=ud)
+                torch.cuda.synchronize()
+                res.append(ud2.cpu().numpy().copy())
+        outs[flag] = res
+    for a, b in zip(outs["0"], outs["1"]):
+        assert np.array_equal(a, b)
+    u_ref, _, _ = h.evaluate(ws[3].astype(np.float64))
+    assert rel2(outs["0"][4].astype(np.float64), u_ref) <= TOL32
+
+
 def test_f32_c3_shaped_sample(gpu, oracle):
     """A c3-shaped tree (d=8, m=s=512, budget .03, r=512) at N=2^15 vs the reference evaluate."""
     from paper_1707_00164_b200 import synth
