@@ -287,6 +287,23 @@ void split_output_parts(Launch& L, const GroupVec& groups, const TileVec& tiles)
   L.parts = std::move(parts);
 }
 
+// Longest-first order of a launch's tiles (ranges [b, e) of a tile list): the block scheduler
+// hands out CTAs roughly in index order, so the long term chains (up to 460 k-stages at c2's leaf
+// level vs a mean of 200) start first instead of forming the launch's tail. Ranges are the
+// output parts (each part must stay row-contiguous) or the whole list.
+template <class GroupVec>
+void order_longest_first(std::vector<Tile>& tiles, int b, int e, const GroupVec& groups) {
+  std::vector<std::pair<int64_t, Tile>> v;
+  v.reserve(size_t(std::max(e - b, 0)));
+  for (int i = b; i < e; ++i) {
+    int64_t w = 0;
+    for (const auto& term : groups[tiles[i].group].terms) w += (term.K + 15) / 16;
+    v.push_back({w, tiles[i]});
+  }
+  std::stable_sort(v.begin(), v.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+  for (int i = b; i < e; ++i) tiles[i] = v[size_t(i - b)].second;
+}
+
 // ---------------------------------------------------------------- subtree-split distribution
 // north_star (4): for P = 2^l GPUs the tree is split at level l into P subtrees, one per rank.
 // Rank g owns the nodes below its level-l node; nodes above level l ("top") are evaluated
@@ -605,6 +622,12 @@ void build_f32(gofmm_handle* H) {
       int t = L.first_tile32;
       while (t < L.first_tile32 + L.ntiles32 && tiles32[t].group < gb) ++t;
       L.parts[p].tile32 = t;
+    }
+    if (L.parts.empty()) {
+      order_longest_first(tiles32, L.first_tile32, L.first_tile32 + L.ntiles32, H->groups);
+    } else {
+      for (size_t p = 0; p + 1 < L.parts.size(); ++p)
+        order_longest_first(tiles32, L.parts[p].tile32, L.parts[p + 1].tile32, H->groups);
     }
   }
   H->d_tiles32.upload(tiles32);
@@ -963,6 +986,14 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
       L.tn[c] = int(H->tiles.size()) - L.tfirst[c];
     }
     if (out == Buf::Out) split_output_parts(L, H->groups, H->tiles);
+    for (int c = 0; c < 3; ++c) {
+      if (L.parts.empty()) {
+        order_longest_first(H->tiles, L.tfirst[c], L.tfirst[c] + L.tn[c], H->groups);
+      } else {
+        for (size_t p = 0; p + 1 < L.parts.size(); ++p)
+          order_longest_first(H->tiles, L.parts[p].tile[c], L.parts[p + 1].tile[c], H->groups);
+      }
+    }
     if (L.tn[0] > 0) H->launches.push_back(std::move(L));
   };
 
