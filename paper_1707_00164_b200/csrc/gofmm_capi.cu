@@ -233,6 +233,9 @@ struct HostGroup {
 struct Launch {
   // FP64 tile lists of this launch's groups, one per tile-row class: kBM[c] rows per tile
   int tfirst[3] = {0, 0, 0}, tn[3] = {0, 0, 0};
+  // k-stages (16-deep) of the tiles' term chains: sum over each tile list, and the longest chain
+  int64_t chain_sum[3] = {0, 0, 0};
+  int64_t chain_max = 0;
   bool gen = false;  // G config (generated operands present)
   Buf out;
   int phase;  // 0 upward, 1 downward, 2 output
@@ -411,6 +414,7 @@ DistPlan make_dist_plan(int nranks, int nn, const int32_t* left, const int32_t* 
 
 struct gofmm_handle {
   int device = 0;
+  int num_sms = 148;  // launch-config costing (queried at create)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
   // host-buffer evaluation pipeline (evaluate_host): H2D / D2H copy streams and, per staging
@@ -985,6 +989,13 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
         for (int m0 = 0; m0 < std::max(H->groups[gi].M, 0); m0 += kBM[c]) H->tiles.push_back({gi, m0});
       L.tn[c] = int(H->tiles.size()) - L.tfirst[c];
     }
+    for (int c = 0; c < 3; ++c)
+      for (int i = L.tfirst[c]; i < L.tfirst[c] + L.tn[c]; ++i) {
+        int64_t w = 0;
+        for (const HostTerm& t : H->groups[H->tiles[i].group].terms) w += (t.K + 15) / 16;
+        L.chain_sum[c] += w;
+        L.chain_max = std::max(L.chain_max, w);
+      }
     if (out == Buf::Out) split_output_parts(L, H->groups, H->tiles);
     for (int c = 0; c < 3; ++c) {
       if (L.parts.empty()) {
@@ -1321,15 +1332,40 @@ struct LaunchCfg {
   const BMaps* maps;
   int bm_class;  // tile list: kBM[bm_class] rows per tile
 };
+// The widest tile that fits r is the most efficient per flop (generated entries and B tiles are
+// amortised over more columns), but a launch with few or very unequal term chains is bounded by
+// its longest chain, which a narrower N tile shortens (and multiplies the CTAs). Each candidate
+// is costed as  (BM*BN / eff) * max(stage-work / SMs, longest chain)  and the cheapest is used:
+// c2's upper downward levels (16-128 groups, chains up to 272 stages) run 64-column tiles.
 LaunchCfg pick_launch_cfg(const gofmm_handle* H, const Launch& L, int32_t r) {
+  struct Cand {
+    LaunchCfg cfg;
+    int bm;
+    double eff;  // achieved fraction of the DMMA peak when the SMs are full (measured, rounded)
+  };
+  Cand c[4];
+  int nc = 0;
   if (!L.gen) {
-    if (r <= 64) return {H->kfn_sn64, H->smem_sn64, 64, &H->maps_n64, 1};
-    return {H->kfn_s, H->smem_s, kBN_S, &H->maps_s, 0};
+    if (r > 64) c[nc++] = {{H->kfn_s, H->smem_s, kBN_S, &H->maps_s, 0}, kBM_S, 0.80};
+    c[nc++] = {{H->kfn_sn64, H->smem_sn64, 64, &H->maps_n64, 1}, kBM_G, 0.60};
+  } else {
+    if (use_wide(r)) c[nc++] = {{H->kfn_gw, H->smem_gw, kBN_GW, &H->maps_g, 2}, kBM_GW, 0.81};
+    if (r > 128) c[nc++] = {{H->kfn_g, H->smem_g, kBN_G, &H->maps_g, 1}, kBM_G, 0.75};
+    if (r > 64) c[nc++] = {{H->kfn_gn128, H->smem_gn128, 128, &H->maps_s, 1}, kBM_G, 0.65};
+    c[nc++] = {{H->kfn_gn64, H->smem_gn64, 64, &H->maps_n64, 1}, kBM_G, 0.55};
   }
-  if (use_wide(r)) return {H->kfn_gw, H->smem_gw, kBN_GW, &H->maps_g, 2};
-  if (r <= 64) return {H->kfn_gn64, H->smem_gn64, 64, &H->maps_n64, 1};
-  if (r <= 128) return {H->kfn_gn128, H->smem_gn128, 128, &H->maps_s, 1};
-  return {H->kfn_g, H->smem_g, kBN_G, &H->maps_g, 1};
+  int best = 0;
+  double best_t = 0.0;
+  for (int i = 0; i < nc; ++i) {
+    const int nt = (r + c[i].cfg.bn - 1) / c[i].cfg.bn;
+    const double work = double(L.chain_sum[c[i].cfg.bm_class]) * nt / double(H->num_sms);
+    const double t = double(c[i].bm) * c[i].cfg.bn / c[i].eff * std::max(work, double(L.chain_max));
+    if (i == 0 || t < best_t) {
+      best = i;
+      best_t = t;
+    }
+  }
+  return c[best].cfg;
 }
 
 // rows_done (host-buffer pipeline, stage 0 only): called after each part of a split output
@@ -1686,6 +1722,7 @@ int gofmm_create(const gofmm_tree_desc* desc, const gofmm_options* opts, gofmm_h
     auto H = std::make_unique<gofmm_handle>();
     H->device = opts ? opts->device : 0;
     GOFMM_CUDA(cudaSetDevice(H->device));
+    GOFMM_CUDA(cudaDeviceGetAttribute(&H->num_sms, cudaDevAttrMultiProcessorCount, H->device));
     GOFMM_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
     for (auto& e : H->ev) GOFMM_CUDA(cudaEventCreate(&e));
     build(H.get(), desc, opts);
@@ -1710,6 +1747,7 @@ int gofmm_create_dist(const gofmm_tree_desc* desc, const gofmm_options* opts, in
     H->drank = rank;
     H->nranks = nranks;
     GOFMM_CUDA(cudaSetDevice(H->device));
+    GOFMM_CUDA(cudaDeviceGetAttribute(&H->num_sms, cudaDevAttrMultiProcessorCount, H->device));
     GOFMM_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
     for (auto& e : H->ev) GOFMM_CUDA(cudaEventCreate(&e));
     build(H.get(), desc, opts);

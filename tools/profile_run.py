@@ -32,3 +32,7 @@ for i in range(a.evals):
     _, st = ev.evaluate_torch(w, out=u, sync_stats=True)
     print(i, {k: round(v, 3) for k, v in st.items()}, ev.phase_flops(r), flush=True)
 print("launches/eval", ev.launches_per_eval, "depth", tree.depth)
+for L in ev.launch_profile(r):
+    tf = L["flops"] / (L["ms"] * 1e-3) / 1e12 if L["ms"] > 0 else 0.0
+    print(f"  {L['phase']:9s} level {L['level']:3d} ctas {L['ctas']:7d} gen {L['generated']} "
+          f"ms {L['ms']:9.3f} TF/s {tf:6.2f}")
