@@ -220,6 +220,28 @@ int gofmm_exact_rows(gofmm_handle* h, const int32_t* rows, int32_t nrows, const 
 int gofmm_rng_eps2_draw(uint64_t seed, int32_t n, int32_t r, int32_t sample_rows, int32_t* rows_out, double* w_out,
                         int64_t ldw);
 
+/* ---- compress-side skeletonisation ------------------------------------
+ * Replaces gfmm::skeletonize_node (compress.hpp:149-187) for a batch of nodes: column-pivoted
+ * Householder QR of each node's sampled block K(sample_cols, candidates) in the reference's
+ * Eigen 3.4 ColPivHouseholderQR operation order, rank = #{l : |R_ll| > tau |R_11|} clamped to
+ * [1, min(s, rows, cols)], skeleton = the first rank pivots, proj = [I | R11^-1 R12] in pivot
+ * order. Bit-identical to the reference on the same block (tests/test_skel_gpu.py).
+ * blocks: node t's block column-major rows[t] x cols[t] at blocks + block_off[t] (host).
+ * Outputs (host): rank_out[t]; achieved_out[t] (Skeleton::achieved_tol); perm_out: cols[t]
+ * column-pivot indices per node, concatenated (skeleton = candidates[perm[0..rank)]);
+ * proj_out: per node a slot of min(s, rows, cols) * cols doubles, concatenated, of which the
+ * first rank * cols hold proj column-major (ld = rank). */
+typedef struct gofmm_skel_stats {
+  double seconds;   /* wall time of the call (uploads, kernel, downloads) */
+  double kernel_ms; /* device time of the batched kernel (CUDA events) */
+  double bytes;     /* algorithmic bytes streamed by the kernel (3 passes over each trailing block) */
+  double flops;     /* Householder application flops (4 per trailing element per step) */
+} gofmm_skel_stats;
+int gofmm_skeletonize_batch(int32_t nnodes, const int32_t* rows, const int32_t* cols, const int64_t* block_off,
+                            const double* blocks, int32_t s, double tau, int32_t device, int32_t* rank_out,
+                            double* achieved_out, int32_t* perm_out, double* proj_out, gofmm_skel_stats* stats);
+const char* gofmm_skeletonize_last_error(void);
+
 /* Bytes of device memory held by the handle (tree + workspace). */
 int64_t gofmm_device_bytes(const gofmm_handle* h);
 

@@ -11,8 +11,11 @@
 // plus export/import of the compressed structure so the GPU product and this oracle consume the
 // SAME tree. Nothing in the product links or loads this library (paper_1707_00164_b200/ never
 // imports oracle/); only tests/, __graft_entry__.smoke() and bench.py's reference legs do.
+#include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <vector>
 #include <exception>
 #include <memory>
 #include <string>
@@ -75,6 +78,24 @@ class ExponentialKernelOracle final : public EntryOracle {
  private:
   PointCloud points_;
   double h_;
+};
+
+/// Serves one given block: rows are sample indices [0, rows), columns are candidates
+/// [rows, rows + cols). Lets skeletonize_node (compress.hpp:149-187) run unmodified on a block
+/// supplied by the test (the GPU batch gets the very same block).
+class GivenBlockOracle final : public EntryOracle {
+ public:
+  GivenBlockOracle(const double* b, int rows, int cols) : b_(b), rows_(rows), cols_(cols) {}
+  int size() const override { return rows_ + cols_; }
+  void eval_block(std::span<const int> I, std::span<const int> J, Matrix& out) const override {
+    out.resize(I.size(), J.size());
+    for (size_t c = 0; c < J.size(); ++c)
+      for (size_t r = 0; r < I.size(); ++r) out(r, c) = b_[size_t(J[c] - rows_) * rows_ + I[r]];
+  }
+
+ private:
+  const double* b_;
+  int rows_, cols_;
 };
 
 }  // namespace
@@ -486,6 +507,36 @@ int gfmm_ref_compress_stats(const gfmm_ref* ref, int64_t* entries, int64_t* cflo
     *max_skel = s.max_skeleton;
     *mean_skel = s.mean_skeleton;
     *cseconds = s.compress_seconds;
+  });
+}
+
+/// The reference skeletonize_node (compress.hpp:149-187) over a batch of given blocks (node t:
+/// column-major rows[t] x cols[t] at blocks + off[t]), parallel over nodes like compress() does
+/// (parallel_for, common.hpp:109-126). Outputs as gofmm_skeletonize_batch: rank, achieved_tol,
+/// skel (pivot index per skeleton entry, slot of cols[t] ints), proj (slot of
+/// min(s, rows, cols) * cols doubles, rank x cols column-major). seconds = wall time of the loop.
+int gfmm_ref_skeletonize_batch(int32_t nnodes, const int32_t* rows, const int32_t* cols, const int64_t* off,
+                               const double* blocks, int32_t s, double tau, int32_t threads, int32_t* rank_out,
+                               double* achieved_out, int32_t* skel_out, double* proj_out, double* seconds) {
+  return guarded([&] {
+    std::vector<int64_t> soff(nnodes + 1, 0), poff(nnodes + 1, 0);
+    for (int t = 0; t < nnodes; ++t) {
+      soff[t + 1] = soff[t] + cols[t];
+      poff[t + 1] = poff[t] + int64_t(std::min({s, rows[t], cols[t]})) * cols[t];
+    }
+    auto t0 = std::chrono::steady_clock::now();
+    parallel_for(0, nnodes, std::max(1, threads), [&](int t) {
+      GivenBlockOracle o(blocks + off[t], rows[t], cols[t]);
+      IndexList sample(rows[t]), cand(cols[t]);
+      for (int i = 0; i < rows[t]; ++i) sample[i] = i;
+      for (int j = 0; j < cols[t]; ++j) cand[j] = rows[t] + j;
+      Skeleton sk = skeletonize_node(t, cand, sample, o, s, tau);
+      rank_out[t] = sk.rank();
+      achieved_out[t] = sk.achieved_tol;
+      for (int l = 0; l < sk.rank(); ++l) skel_out[soff[t] + l] = sk.skel[l] - rows[t];
+      for (int64_t e = 0; e < int64_t(sk.rank()) * cols[t]; ++e) proj_out[poff[t] + e] = sk.proj.data()[e];
+    });
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
 }
 

@@ -135,6 +135,8 @@ def lib():
                                           C.POINTER(C.c_double), _P]
         L.gfmm_ref_eps2_draw.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_uint64, _P, _P]
         L.gfmm_ref_compress_stats.argtypes = [_P] + [_P] * 6
+        L.gfmm_ref_skeletonize_batch.argtypes = [C.c_int32, _P, _P, _P, _P, C.c_int32, C.c_double, C.c_int32,
+                                                 _P, _P, _P, _P, C.POINTER(C.c_double)]
         _lib = L
     return _lib
 
@@ -377,3 +379,32 @@ def import_flat(f: Flat, threads: int = 1) -> RefHMatrix:
     h = C.c_void_p()
     _check(lib().gfmm_ref_import(C.byref(a), C.byref(h)))
     return RefHMatrix(h, f.kernel, f.kparams)
+
+
+def skeletonize_batch(blocks, s: int, tau: float, threads: int = 1):
+    """The reference skeletonize_node (compress.hpp:149-187) on given blocks (rows x cols):
+    list of (rank, skel pivot columns, proj rank x cols, achieved_tol), and the wall seconds."""
+    n = len(blocks)
+    rows = np.array([b.shape[0] for b in blocks], dtype=np.int32)
+    cols = np.array([b.shape[1] for b in blocks], dtype=np.int32)
+    off = np.zeros(n, dtype=np.int64)
+    if n:
+        off[1:] = np.cumsum(rows.astype(np.int64) * cols)[:-1]
+    blob = np.concatenate([np.asfortranarray(b, dtype=np.float64).ravel(order="F") for b in blocks])
+    maxr = np.minimum(np.minimum(rows, cols), s).astype(np.int64)
+    skel = np.zeros(int(cols.sum()), dtype=np.int32)
+    proj = np.zeros(max(int((maxr * cols).sum()), 1), dtype=np.float64)
+    rank = np.zeros(n, dtype=np.int32)
+    ach = np.zeros(n, dtype=np.float64)
+    sec = C.c_double(0.0)
+    _check(lib().gfmm_ref_skeletonize_batch(n, _ptr(rows), _ptr(cols), _ptr(off), _ptr(blob), int(s), float(tau),
+                                            int(threads), _ptr(rank), _ptr(ach), _ptr(skel), _ptr(proj),
+                                            C.byref(sec)))
+    out, so, pp = [], 0, 0
+    for t in range(n):
+        k, c = int(rank[t]), int(cols[t])
+        out.append((k, skel[so:so + k].copy(), proj[pp:pp + k * c].reshape((k, c), order="F").copy(),
+                    float(ach[t])))
+        so += c
+        pp += int(maxr[t]) * c
+    return out, sec.value

@@ -36,8 +36,8 @@ BLOCKS_MATERIALIZE = 1
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC"]
 # translation units of the library, compiled in parallel then linked: the C-ABI + FP64 DMMA
-# kernels, and the FP32 3xTF32 tcgen05 kernels
-UNITS = ("gofmm_capi.cu", "gofmm_f32.cu")
+# kernels, the FP32 3xTF32 tcgen05 kernels, and the compress-side batched skeletonisation
+UNITS = ("gofmm_capi.cu", "gofmm_f32.cu", "gofmm_skel.cu")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -132,7 +132,12 @@ EXPORTS = ("gofmm_create", "gofmm_evaluate", "gofmm_evaluate_device", "gofmm_unp
            "gofmm_last_error", "gofmm_abi_version", "gofmm_create_dist", "gofmm_dist_get_info",
            "gofmm_dist_plan_host", "gofmm_dist_stage1", "gofmm_dist_stage2", "gofmm_exact_rows",
            "gofmm_rng_eps2_draw", "gofmm_evaluate_f32", "gofmm_evaluate_device_f32",
-           "gofmm_unpermute_device_f32", "gofmm_precision", "gofmm_dist_stage1_f32", "gofmm_dist_stage2_f32")
+           "gofmm_unpermute_device_f32", "gofmm_precision", "gofmm_dist_stage1_f32", "gofmm_dist_stage2_f32",
+           "gofmm_skeletonize_batch", "gofmm_skeletonize_last_error")
+
+
+class SkelStats(C.Structure):
+    _fields_ = [("seconds", C.c_double), ("kernel_ms", C.c_double), ("bytes", C.c_double), ("flops", C.c_double)]
 
 
 def lib():
@@ -170,6 +175,9 @@ def lib():
         L.gofmm_launches_per_eval.argtypes = [P]
         L.gofmm_destroy.argtypes = [P]
         L.gofmm_last_error.restype = C.c_char_p
+        L.gofmm_skeletonize_batch.argtypes = [C.c_int32, P, P, P, P, C.c_int32, C.c_double, C.c_int32, P, P, P, P,
+                                              C.POINTER(SkelStats)]
+        L.gofmm_skeletonize_last_error.restype = C.c_char_p
         _lib = L
     return _lib
 
