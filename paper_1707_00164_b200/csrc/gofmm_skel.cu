@@ -28,7 +28,7 @@
 
 namespace gofmm_skel {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 128;  // 4 CTAs (nodes) per SM: one node's serial pivot phase overlaps the others' streaming
 
 struct NodeDesc {
   int64_t in_off;    // block (column-major rows x cols) in the input blob
@@ -73,21 +73,57 @@ __device__ double redux_packet(int n, F get) {
   return res;
 }
 
-// Row-major GEMV dot of Eigen's general_matrix_vector_product (eigen_shim gemv_dot, Dense:92-102)
+// The same reduction split over lanes 0..3 of one warp (one packet accumulator chain each, the
+// exact element-to-chain assignment of redux_packet), combined on lane 0 in the same order.
+// get() must be cheap (shared memory): the chains are latency-bound otherwise. Lane 0 returns it.
 template <class F>
-__device__ double gemv_dot(int n, F prod) {
+__device__ double redux_packet_lanes(int n, F get, int lane) {
+  const int aligned = (n / 2) * 2, aligned2 = (n / 4) * 4;
+  if (aligned <= 2) return lane == 0 ? redux_packet(n, get) : 0.0;
+  double acc = 0.0;
+  if (lane < 4) {
+    acc = get(lane);
+    for (int i = 4 + lane; i < aligned2; i += 4) acc = add(acc, get(i));
+  }
+  const double a1 = __shfl_sync(0xffffffffu, acc, 1), b0 = __shfl_sync(0xffffffffu, acc, 2),
+               b1 = __shfl_sync(0xffffffffu, acc, 3);
+  if (lane != 0) return 0.0;
+  double x0 = add(acc, b0), x1 = add(a1, b1);
+  if (aligned > aligned2) {
+    x0 = add(x0, get(aligned2));
+    x1 = add(x1, get(aligned2 + 1));
+  }
+  double res = add(x0, x1);
+  for (int i = aligned; i < n; ++i) res = add(res, get(i));
+  return res;
+}
+
+// Row-major GEMV dot of Eigen's general_matrix_vector_product (eigen_shim gemv_dot, Dense:92-102):
+// sum_i col[i*ld] * v[i] with even / odd accumulators. Loads are issued 8 rows ahead of the
+// (order-preserving) adds so one thread keeps several global loads in flight.
+__device__ double gemv_dot_col(int n, const double* __restrict__ col, int64_t ld, const double* __restrict__ v) {
   double c0 = 0.0, c1 = 0.0;
   int j = 0;
+  for (; j + 8 <= n; j += 8) {
+    double x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = col[int64_t(j + u) * ld];
+#pragma unroll
+    for (int u = 0; u < 8; u += 2) {
+      c0 = add(c0, mul(x[u], v[j + u]));
+      c1 = add(c1, mul(x[u + 1], v[j + u + 1]));
+    }
+  }
   for (; j + 2 <= n; j += 2) {
-    c0 = add(c0, prod(j));
-    c1 = add(c1, prod(j + 1));
+    c0 = add(c0, mul(col[int64_t(j) * ld], v[j]));
+    c1 = add(c1, mul(col[int64_t(j + 1) * ld], v[j + 1]));
   }
   double cc = add(c0, c1);
-  for (; j < n; ++j) cc = add(cc, prod(j));
+  for (; j < n; ++j) cc = add(cc, mul(col[int64_t(j) * ld], v[j]));
   return cc;
 }
 
-__global__ void __launch_bounds__(kThreads) skeletonize_kernel(const NodeDesc* __restrict__ nodes,
+__global__ void __launch_bounds__(kThreads, 4) skeletonize_kernel(const NodeDesc* __restrict__ nodes,
                                                                const double* __restrict__ in, double* __restrict__ ws,
                                                                int32_t s_max, double tau_tol,
                                                                int32_t* __restrict__ rank_out,
@@ -95,7 +131,7 @@ __global__ void __launch_bounds__(kThreads) skeletonize_kernel(const NodeDesc* _
                                                                int32_t* __restrict__ perm_out,
                                                                double* __restrict__ proj_out) {
   const NodeDesc nd = nodes[blockIdx.x];
-  const int rows = nd.rows, cols = nd.cols, ld = cols;
+  const int rows = nd.rows, cols = nd.cols, ld = (cols + 1) & ~1;  // even: 16-byte column pairs
   const int size = min(rows, cols);
   double* A = ws + nd.ws_off;  // A(i, j) = A[i * ld + j]
   extern __shared__ double sh[];
@@ -112,7 +148,7 @@ __global__ void __launch_bounds__(kThreads) skeletonize_kernel(const NodeDesc* _
   // column-major input -> row-major workspace
   for (int64_t e = tid; e < int64_t(rows) * cols; e += blockDim.x) {
     const int i = int(e / cols), j = int(e % cols);
-    A[e] = in[nd.in_off + int64_t(j) * rows + i];
+    A[int64_t(i) * ld + j] = in[nd.in_off + int64_t(j) * rows + i];
   }
   __syncthreads();
   // initial column norms: col(k).norm() (ColPivHouseholderQR::computeInPlace)
@@ -177,15 +213,16 @@ __global__ void __launch_bounds__(kThreads) skeletonize_kernel(const NodeDesc* _
         A[int64_t(i) * ld + big] = t;
       }
     __syncthreads();
-    // (2) makeHouseholderInPlace on column k, rows k..rows-1
+    // (2) makeHouseholderInPlace on column k, rows k..rows-1: the column is staged in shared
+    // memory (ess[i] = A(k+1+i, k)) by all threads, its tail norm reduced by 4 lanes
     const int len = rows - k;
-    if (tid == 0) {
+    for (int i = 1 + tid; i < len; i += blockDim.x) ess[i - 1] = A[int64_t(k + i) * ld + k];
+    __syncthreads();
+    if (tid < 32) {
       double tail_sq = 0.0;
       if (len > 1)
-        tail_sq = redux_packet(len - 1, [&](int i) {
-          const double v = A[int64_t(k + 1 + i) * ld + k];
-          return mul(v, v);
-        });
+        tail_sq = redux_packet_lanes(len - 1, [&](int i) { return mul(ess[i], ess[i]); }, tid);
+      if (tid == 0) {
       const double c0 = A[int64_t(k) * ld + k];
       double tau, beta, denom = 0.0;
       if (tail_sq <= DBL_MIN) {
@@ -200,36 +237,100 @@ __global__ void __launch_bounds__(kThreads) skeletonize_kernel(const NodeDesc* _
       s_tau = tau;
       s_beta = beta;
       s_denom = denom;
+      }
     }
     __syncthreads();
     const double tau = s_tau;
     for (int i = 1 + tid; i < len; i += blockDim.x) {
-      double* p = &A[int64_t(k + i) * ld + k];
-      const double v = (tau == 0.0 && s_denom == 0.0) ? 0.0 : __ddiv_rn(*p, s_denom);
-      *p = v;
+      const double v = (tau == 0.0 && s_denom == 0.0) ? 0.0 : __ddiv_rn(ess[i - 1], s_denom);
+      A[int64_t(k + i) * ld + k] = v;
       ess[i - 1] = v;
       tess[i - 1] = mul(tau, v);
     }
     if (tid == 0) A[int64_t(k) * ld + k] = s_beta;
     __syncthreads();
-    // (3) applyHouseholderOnTheLeft on the trailing columns, one thread per column
+    // (3) applyHouseholderOnTheLeft on the trailing columns. A thread owns an aligned column
+    // PAIR (2p, 2p+1) and streams both with 16-byte loads, 8 rows ahead of the order-preserving
+    // accumulation, so each SM keeps enough bytes in flight to approach its HBM share.
     const int nc = cols - k - 1, m1 = len - 1;
-    for (int j = k + 1 + tid; j < cols; j += blockDim.x) {
-      double* top = &A[int64_t(k) * ld + j];
-      if (len == 1) {
-        *top = mul(*top, sub(1.0, tau));
-      } else if (tau != 0.0) {
-        const double* bcol = &A[int64_t(k + 1) * ld + j];
-        double t = (nc == 1) ? redux_packet(m1, [&](int i) { return mul(ess[i], bcol[int64_t(i) * ld]); })
-                             : gemv_dot(m1, [&](int i) { return mul(bcol[int64_t(i) * ld], ess[i]); });
-        t = add(t, *top);
-        *top = sub(*top, mul(tau, t));
-        double* bw = &A[int64_t(k + 1) * ld + j];
-        for (int i = 0; i < m1; ++i) bw[int64_t(i) * ld] = sub(bw[int64_t(i) * ld], mul(t, tess[i]));
+    if (len == 1 || tau == 0.0 || nc == 1) {
+      for (int j = k + 1 + tid; j < cols; j += blockDim.x) {
+        double* top = &A[int64_t(k) * ld + j];
+        if (len == 1) {
+          *top = mul(*top, sub(1.0, tau));
+        } else if (tau != 0.0) {  // nc == 1: a single column falls back to an inner product
+          double* bcol = &A[int64_t(k + 1) * ld + j];
+          double t = redux_packet(m1, [&](int i) { return mul(ess[i], bcol[int64_t(i) * ld]); });
+          t = add(t, *top);
+          *top = sub(*top, mul(tau, t));
+          for (int i = 0; i < m1; ++i) bcol[int64_t(i) * ld] = sub(bcol[int64_t(i) * ld], mul(t, tess[i]));
+        }
       }
-      // (4) LAPACK-style column-norm downdate (lawn176)
+    } else {
+      for (int pr = ((k + 1) >> 1) + tid; 2 * pr < cols; pr += blockDim.x) {
+        const int j0 = 2 * pr;
+        const bool act0 = j0 > k, act1 = j0 + 1 > k && j0 + 1 < cols;
+        const double* b = &A[int64_t(k + 1) * ld + j0];
+        double c0a = 0.0, c1a = 0.0, c0b = 0.0, c1b = 0.0;
+        int i = 0;
+        for (; i + 8 <= m1; i += 8) {
+          double2 x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) x[u] = *reinterpret_cast<const double2*>(b + int64_t(i + u) * ld);
+#pragma unroll
+          for (int u = 0; u < 8; u += 2) {
+            c0a = add(c0a, mul(x[u].x, ess[i + u]));
+            c1a = add(c1a, mul(x[u + 1].x, ess[i + u + 1]));
+            c0b = add(c0b, mul(x[u].y, ess[i + u]));
+            c1b = add(c1b, mul(x[u + 1].y, ess[i + u + 1]));
+          }
+        }
+        for (; i + 2 <= m1; i += 2) {
+          const double2 x0 = *reinterpret_cast<const double2*>(b + int64_t(i) * ld);
+          const double2 x1 = *reinterpret_cast<const double2*>(b + int64_t(i + 1) * ld);
+          c0a = add(c0a, mul(x0.x, ess[i]));
+          c1a = add(c1a, mul(x1.x, ess[i + 1]));
+          c0b = add(c0b, mul(x0.y, ess[i]));
+          c1b = add(c1b, mul(x1.y, ess[i + 1]));
+        }
+        double ta = add(c0a, c1a), tb = add(c0b, c1b);
+        for (; i < m1; ++i) {
+          const double2 x0 = *reinterpret_cast<const double2*>(b + int64_t(i) * ld);
+          ta = add(ta, mul(x0.x, ess[i]));
+          tb = add(tb, mul(x0.y, ess[i]));
+        }
+        double* top = &A[int64_t(k) * ld + j0];
+        if (act0) {
+          ta = add(ta, top[0]);
+          top[0] = sub(top[0], mul(tau, ta));
+        }
+        if (act1) {
+          tb = add(tb, top[1]);
+          top[1] = sub(top[1], mul(tau, tb));
+        }
+        double* bw = &A[int64_t(k + 1) * ld + j0];
+        if (act0 && act1) {
+#pragma unroll 8
+          for (int r = 0; r < m1; ++r) {
+            double2 v = *reinterpret_cast<double2*>(bw + int64_t(r) * ld);
+            v.x = sub(v.x, mul(ta, tess[r]));
+            v.y = sub(v.y, mul(tb, tess[r]));
+            *reinterpret_cast<double2*>(bw + int64_t(r) * ld) = v;
+          }
+        } else {
+          double* c = bw + (act0 ? 0 : 1);
+          const double t = act0 ? ta : tb;
+#pragma unroll 8
+          for (int r = 0; r < m1; ++r) c[int64_t(r) * ld] = sub(c[int64_t(r) * ld], mul(t, tess[r]));
+        }
+      }
+    }
+    __syncthreads();
+    // (4) LAPACK-style column-norm downdate (lawn176), one thread per column
+    for (int j = k + 1 + tid; j < cols; j += blockDim.x) {
       if (upd[j] != 0.0) {
-        double t = __ddiv_rn(fabs(*top), upd[j]);
+        const double top = A[int64_t(k) * ld + j];
+        double t = __ddiv_rn(fabs(top), upd[j]);
         t = mul(add(1.0, t), sub(1.0, t));
         t = t < 0.0 ? 0.0 : t;
         const double ratio = __ddiv_rn(upd[j], direct[j]);
@@ -335,7 +436,7 @@ int gofmm_skeletonize_batch(int32_t nnodes, const int32_t* rows, const int32_t* 
       return skel_fail(GOFMM_ERR_INVALID, "skeletonize_batch: every node needs rows, cols >= 1");
     nd[t] = {block_off[t], ws, pe, pj, rows[t], cols[t]};
     in_elems = std::max(in_elems, block_off[t] + int64_t(rows[t]) * cols[t]);
-    ws += int64_t(rows[t]) * cols[t];
+    ws += int64_t(rows[t]) * ((cols[t] + 1) & ~1);  // row-major, even ld (kernel)
     pe += cols[t];
     pj += int64_t(std::min({s, rows[t], cols[t]})) * cols[t];
     max_rows = std::max(max_rows, int(rows[t]));
