@@ -17,7 +17,11 @@ hdr_i = next(i for i, r in enumerate(rows) if "Source" in r and "Address" in r)
 h = rows[hdr_i]
 ix = {k: i for i, k in enumerate(h)}
 S = "Warp Stall Sampling (All Samples)"
-data = [r for r in rows[hdr_i + 1:] if len(r) == len(h) and r[0] != "Address"]
+data, seen = [], set()
+for r in rows[hdr_i + 1:]:
+    if len(r) == len(h) and r[0] != "Address" and r[0] not in seen:  # the page repeats each address
+        seen.add(r[0])
+        data.append(r)
 tot = sum(f(r[ix[S]]) for r in data) or 1.0
 reasons = [k for k in h if k.startswith("stall_") and "Not Issued" not in k]
 top = sorted(data, key=lambda r: -f(r[ix[S]]))[: int(sys.argv[2]) if len(sys.argv) > 2 else 40]
