@@ -242,6 +242,19 @@ int gofmm_skeletonize_batch(int32_t nnodes, const int32_t* rows, const int32_t* 
                             double* achieved_out, int32_t* perm_out, double* proj_out, gofmm_skel_stats* stats);
 const char* gofmm_skeletonize_last_error(void);
 
+/* ---- ANN leaf pass -----------------------------------------------------
+ * The per-leaf body of ann_iteration (neighbors.hpp:88-106) for all leaves of one random tree:
+ * pairwise distances inside each leaf (kind 0: GeometricL2, bit-identical to the reference;
+ * kind 1: KernelL2 over a Gaussian oracle of bandwidth h) merged into every index's list as the
+ * kappa smallest distinct indices under (distance, index) (merge_candidates, :35-63).
+ * coords: d x n column-major (host). Leaves: leaf_idx[leaf_off[l] .. leaf_off[l+1]) (host; from
+ * the host-built random tree). Table (host, updated in place): table_j / table_d n x kappa
+ * row-major, table_len[i] entries valid. kappa = NeighborTable::k (<= 32); leaves <= 1024. */
+int gofmm_ann_leaf_merge(int32_t n, int32_t d, const double* coords, int32_t kind, double h, int32_t kappa,
+                         int32_t nleaves, const int32_t* leaf_off, const int32_t* leaf_idx, int32_t device,
+                         int32_t* table_j, double* table_d, int32_t* table_len, double* kernel_ms);
+const char* gofmm_ann_last_error(void);
+
 /* Bytes of device memory held by the handle (tree + workspace). */
 int64_t gofmm_device_bytes(const gofmm_handle* h);
 

@@ -540,4 +540,58 @@ int gfmm_ref_skeletonize_batch(int32_t nnodes, const int32_t* rows, const int32_
   });
 }
 
+// ---- ANN (neighbors.hpp:88-106): the random tree's leaves and one reference ann_iteration on a
+// given table, for the GPU leaf all-pairs + merge parity (tests/test_ann_gpu.py).
+// kind: 0 = GeometricL2, 1 = KernelL2 over a Gaussian oracle of bandwidth h (metric.hpp).
+struct AnnCtx {
+  PointCloud pc;
+  std::unique_ptr<EntryOracle> oracle;
+  std::unique_ptr<Metric> metric;
+  AnnCtx(const double* coords, int32_t d, int32_t n, int32_t kind, double h) {
+    pc.coords.resize(d, n);
+    std::memcpy(pc.coords.data(), coords, sizeof(double) * size_t(d) * size_t(n));
+    oracle = std::make_unique<GaussianKernelOracle>(pc, h);
+    metric = std::make_unique<Metric>(kind == 0 ? DistanceKind::GeometricL2 : DistanceKind::KernelL2, *oracle,
+                                      &pc);
+  }
+};
+
+int gfmm_ref_ann_leaves(const double* coords, int32_t d, int32_t n, int32_t kind, double h, int32_t m,
+                        uint64_t seed, int32_t* leaf_off, int32_t* leaf_idx, int32_t* nleaves) {
+  return guarded([&] {
+    AnnCtx c(coords, d, n, kind, h);
+    MetricTree tree = build_random_tree(*c.metric, m, seed);
+    int pos = 0;
+    leaf_off[0] = 0;
+    for (size_t l = 0; l < tree.leaf_ids.size(); ++l) {
+      IndexList idx = tree.node_indices(tree.leaf_ids[l]);
+      for (int i : idx) leaf_idx[pos++] = i;
+      leaf_off[l + 1] = pos;
+    }
+    *nleaves = int32_t(tree.leaf_ids.size());
+  });
+}
+
+int gfmm_ref_ann_iteration(const double* coords, int32_t d, int32_t n, int32_t kind, double h, int32_t kappa,
+                           int32_t m, uint64_t seed, int32_t threads, int32_t* tj, double* td, int32_t* tlen,
+                           double* seconds) {
+  return guarded([&] {
+    AnnCtx c(coords, d, n, kind, h);
+    NeighborTable table = NeighborTable::empty(n, kappa);
+    for (int i = 0; i < n; ++i)
+      for (int t = 0; t < tlen[i]; ++t)
+        table.lists[i].emplace_back(tj[size_t(i) * kappa + t], td[size_t(i) * kappa + t]);
+    auto t0 = std::chrono::steady_clock::now();
+    ann_iteration(table, *c.metric, m, seed, std::max(1, threads));
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (int i = 0; i < n; ++i) {
+      tlen[i] = int32_t(table.lists[i].size());
+      for (int t = 0; t < tlen[i]; ++t) {
+        tj[size_t(i) * kappa + t] = table.lists[i][t].first;
+        td[size_t(i) * kappa + t] = table.lists[i][t].second;
+      }
+    }
+  });
+}
+
 }  // extern "C"

@@ -135,6 +135,10 @@ def lib():
                                           C.POINTER(C.c_double), _P]
         L.gfmm_ref_eps2_draw.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_uint64, _P, _P]
         L.gfmm_ref_compress_stats.argtypes = [_P] + [_P] * 6
+        L.gfmm_ref_ann_leaves.argtypes = [_P, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_uint64,
+                                          _P, _P, _P]
+        L.gfmm_ref_ann_iteration.argtypes = [_P, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int32,
+                                             C.c_int32, C.c_uint64, C.c_int32, _P, _P, _P, C.POINTER(C.c_double)]
         L.gfmm_ref_skeletonize_batch.argtypes = [C.c_int32, _P, _P, _P, _P, C.c_int32, C.c_double, C.c_int32,
                                                  _P, _P, _P, _P, C.POINTER(C.c_double)]
         _lib = L
@@ -408,3 +412,27 @@ def skeletonize_batch(blocks, s: int, tau: float, threads: int = 1):
         so += c
         pp += int(maxr[t]) * c
     return out, sec.value
+
+
+def ann_leaves(coords: np.ndarray, kind: int, h: float, m: int, seed: int):
+    """Leaves of build_random_tree(metric, m, seed) (tree.hpp:244-247) as (leaf_off, leaf_idx)."""
+    d, n = coords.shape
+    cf = np.asfortranarray(coords, dtype=np.float64)
+    off = np.zeros(n + 1, dtype=np.int32)
+    idx = np.zeros(n, dtype=np.int32)
+    nl = C.c_int32(0)
+    _check(lib().gfmm_ref_ann_leaves(_ptr(cf), d, n, int(kind), float(h), int(m), C.c_uint64(seed),
+                                     _ptr(off), _ptr(idx), C.byref(nl)))
+    return off[:nl.value + 1].copy(), idx
+
+
+def ann_iteration(coords: np.ndarray, kind: int, h: float, kappa: int, m: int, seed: int, tj, td, tlen,
+                  threads: int = 1) -> float:
+    """One reference ann_iteration (neighbors.hpp:88-106) on the table (tj, td: n x kappa, tlen: n),
+    updated in place; returns the wall seconds."""
+    d, n = coords.shape
+    cf = np.asfortranarray(coords, dtype=np.float64)
+    sec = C.c_double(0.0)
+    _check(lib().gfmm_ref_ann_iteration(_ptr(cf), d, n, int(kind), float(h), int(kappa), int(m), C.c_uint64(seed),
+                                        int(threads), _ptr(tj), _ptr(td), _ptr(tlen), C.byref(sec)))
+    return sec.value

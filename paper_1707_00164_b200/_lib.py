@@ -36,8 +36,8 @@ BLOCKS_MATERIALIZE = 1
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC"]
 # translation units of the library, compiled in parallel then linked: the C-ABI + FP64 DMMA
-# kernels, the FP32 3xTF32 tcgen05 kernels, and the compress-side batched skeletonisation
-UNITS = ("gofmm_capi.cu", "gofmm_f32.cu", "gofmm_skel.cu")
+# kernels, the FP32 3xTF32 tcgen05 kernels, and the compress-side batched skeletonisation and ANN pass
+UNITS = ("gofmm_capi.cu", "gofmm_f32.cu", "gofmm_skel.cu", "gofmm_ann.cu")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -133,7 +133,8 @@ EXPORTS = ("gofmm_create", "gofmm_evaluate", "gofmm_evaluate_device", "gofmm_unp
            "gofmm_dist_plan_host", "gofmm_dist_stage1", "gofmm_dist_stage2", "gofmm_exact_rows",
            "gofmm_rng_eps2_draw", "gofmm_evaluate_f32", "gofmm_evaluate_device_f32",
            "gofmm_unpermute_device_f32", "gofmm_precision", "gofmm_dist_stage1_f32", "gofmm_dist_stage2_f32",
-           "gofmm_skeletonize_batch", "gofmm_skeletonize_last_error")
+           "gofmm_skeletonize_batch", "gofmm_skeletonize_last_error", "gofmm_ann_leaf_merge",
+           "gofmm_ann_last_error")
 
 
 class SkelStats(C.Structure):
@@ -178,6 +179,9 @@ def lib():
         L.gofmm_skeletonize_batch.argtypes = [C.c_int32, P, P, P, P, C.c_int32, C.c_double, C.c_int32, P, P, P, P,
                                               C.POINTER(SkelStats)]
         L.gofmm_skeletonize_last_error.restype = C.c_char_p
+        L.gofmm_ann_leaf_merge.argtypes = [C.c_int32, C.c_int32, P, C.c_int32, C.c_double, C.c_int32, C.c_int32,
+                                           P, P, C.c_int32, P, P, P, C.POINTER(C.c_double)]
+        L.gofmm_ann_last_error.restype = C.c_char_p
         _lib = L
     return _lib
 
