@@ -207,22 +207,19 @@ int gofmm_ann_leaf_merge(int32_t n, int32_t d, const double* coords, int32_t kin
     return ann_fail(GOFMM_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return ann_fail(GOFMM_ERR_CUDA, "cudaSetDevice", e);
-  // coordinates point-major (d doubles per point) for the leaf staging loads
-  std::vector<double> pm(size_t(n) * d);
-  for (int i = 0; i < n; ++i)
-    for (int q = 0; q < d; ++q) pm[size_t(i) * d + q] = coords[size_t(i) * d + q];
   ABuf dc, dlo, dli, dtj, dtd, dtl;
   const size_t nk = size_t(n) * kappa;
-  if ((e = cudaMalloc(&dc.p, pm.size() * 8)) != cudaSuccess || (e = cudaMalloc(&dlo.p, size_t(nleaves + 1) * 4)) ||
+  if ((e = cudaMalloc(&dc.p, size_t(n) * d * 8)) != cudaSuccess || (e = cudaMalloc(&dlo.p, size_t(nleaves + 1) * 4)) ||
       (e = cudaMalloc(&dli.p, size_t(n) * 4)) || (e = cudaMalloc(&dtj.p, nk * 4)) || (e = cudaMalloc(&dtd.p, nk * 8)) ||
       (e = cudaMalloc(&dtl.p, size_t(n) * 4)))
     return ann_fail(GOFMM_ERR_CUDA, "ann_leaf_merge: device allocation", e);
-  cudaMemcpy(dc.p, pm.data(), pm.size() * 8, cudaMemcpyHostToDevice);
-  cudaMemcpy(dlo.p, leaf_off, size_t(nleaves + 1) * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(dli.p, leaf_idx, size_t(leaf_off[nleaves]) * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(dtj.p, table_j, nk * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(dtd.p, table_d, nk * 8, cudaMemcpyHostToDevice);
-  cudaMemcpy(dtl.p, table_len, size_t(n) * 4, cudaMemcpyHostToDevice);
+  if ((e = cudaMemcpy(dc.p, coords, size_t(n) * d * 8, cudaMemcpyHostToDevice))  // d x n column-major = point-major != cudaSuccess ||
+      (e = cudaMemcpy(dlo.p, leaf_off, size_t(nleaves + 1) * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(dli.p, leaf_idx, size_t(leaf_off[nleaves]) * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(dtj.p, table_j, nk * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(dtd.p, table_d, nk * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(dtl.p, table_len, size_t(n) * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+    return ann_fail(GOFMM_ERR_CUDA, "ann_leaf_merge: upload", e);
   const double inv = 1.0 / (2.0 * h * h);  // GaussianKernelOracle::eval_block (oracle.hpp:150)
   const size_t smem = size_t(maxleaf) * d * 8;
   cudaEvent_t ev[2];
@@ -251,10 +248,10 @@ int gofmm_ann_leaf_merge(int32_t n, int32_t d, const double* coords, int32_t kin
   cudaEventDestroy(ev[1]);
   if (e != cudaSuccess) return ann_fail(GOFMM_ERR_CUDA, "ann_leaf_merge: kernel", e);
   if (kernel_ms) *kernel_ms = ms;
-  cudaMemcpy(table_j, dtj.p, nk * 4, cudaMemcpyDeviceToHost);
-  cudaMemcpy(table_d, dtd.p, nk * 8, cudaMemcpyDeviceToHost);
-  e = cudaMemcpy(table_len, dtl.p, size_t(n) * 4, cudaMemcpyDeviceToHost);
-  if (e != cudaSuccess) return ann_fail(GOFMM_ERR_CUDA, "ann_leaf_merge: download", e);
+  if ((e = cudaMemcpy(table_j, dtj.p, nk * 4, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+      (e = cudaMemcpy(table_d, dtd.p, nk * 8, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+      (e = cudaMemcpy(table_len, dtl.p, size_t(n) * 4, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return ann_fail(GOFMM_ERR_CUDA, "ann_leaf_merge: download", e);
   return GOFMM_OK;
 }
 

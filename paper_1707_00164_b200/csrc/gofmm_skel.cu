@@ -455,9 +455,14 @@ int gofmm_skeletonize_batch(int32_t nnodes, const int32_t* rows, const int32_t* 
   cudaEventCreate(&ev[0]);
   cudaEventCreate(&ev[1]);
   auto t0 = std::chrono::steady_clock::now();
-  cudaMemcpy(d_nd.p, nd.data(), nd.size() * sizeof(NodeDesc), cudaMemcpyHostToDevice);
-  cudaMemcpy(d_in.p, blocks, size_t(in_elems) * 8, cudaMemcpyHostToDevice);
-  cudaFuncSetAttribute(skeletonize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if ((e = cudaMemcpy(d_nd.p, nd.data(), nd.size() * sizeof(NodeDesc), cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(d_in.p, blocks, size_t(in_elems) * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(skeletonize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) !=
+          cudaSuccess) {
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    return skel_fail(GOFMM_ERR_CUDA, "skeletonize_batch: upload", e);
+  }
   cudaEventRecord(ev[0]);
   skeletonize_kernel<<<unsigned(nnodes), kThreads, smem>>>(
       static_cast<NodeDesc*>(d_nd.p), static_cast<double*>(d_in.p), static_cast<double*>(d_ws.p), s, tau,
@@ -475,12 +480,12 @@ int gofmm_skeletonize_batch(int32_t nnodes, const int32_t* rows, const int32_t* 
   cudaEventElapsedTime(&ms, ev[0], ev[1]);
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
-  cudaMemcpy(rank_out, d_rank.p, size_t(nnodes) * 4, cudaMemcpyDeviceToHost);
-  cudaMemcpy(achieved_out, d_ach.p, size_t(nnodes) * 8, cudaMemcpyDeviceToHost);
-  cudaMemcpy(perm_out, d_perm.p, size_t(pe) * 4, cudaMemcpyDeviceToHost);
   // proj: per node maxrank x cols slot, of which rank x cols (ld = rank) is written
-  e = cudaMemcpy(proj_out, d_proj.p, size_t(pj) * 8, cudaMemcpyDeviceToHost);
-  if (e != cudaSuccess) return skel_fail(GOFMM_ERR_CUDA, "skeletonize_batch: download", e);
+  if ((e = cudaMemcpy(rank_out, d_rank.p, size_t(nnodes) * 4, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+      (e = cudaMemcpy(achieved_out, d_ach.p, size_t(nnodes) * 8, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+      (e = cudaMemcpy(perm_out, d_perm.p, size_t(pe) * 4, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+      (e = cudaMemcpy(proj_out, d_proj.p, size_t(pj) * 8, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return skel_fail(GOFMM_ERR_CUDA, "skeletonize_batch: download", e);
   if (stats) {
     stats->kernel_ms = ms;
     stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
