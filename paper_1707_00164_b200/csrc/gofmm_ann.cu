@@ -213,7 +213,8 @@ int gofmm_ann_leaf_merge(int32_t n, int32_t d, const double* coords, int32_t kin
       (e = cudaMalloc(&dli.p, size_t(n) * 4)) || (e = cudaMalloc(&dtj.p, nk * 4)) || (e = cudaMalloc(&dtd.p, nk * 8)) ||
       (e = cudaMalloc(&dtl.p, size_t(n) * 4)))
     return ann_fail(GOFMM_ERR_CUDA, "ann_leaf_merge: device allocation", e);
-  if ((e = cudaMemcpy(dc.p, coords, size_t(n) * d * 8, cudaMemcpyHostToDevice))  // d x n column-major = point-major != cudaSuccess ||
+  // coords: d x n column-major is already point-major (d doubles per point)
+  if ((e = cudaMemcpy(dc.p, coords, size_t(n) * d * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(dlo.p, leaf_off, size_t(nleaves + 1) * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(dli.p, leaf_idx, size_t(leaf_off[nleaves]) * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(dtj.p, table_j, nk * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
