@@ -28,8 +28,7 @@
 namespace gofmm_ann {
 
 constexpr int kWarps = 8;
-constexpr int kMaxLeaf = 1024;  // candidates per lane: kMaxLeaf / 32
-constexpr int kPerLane = kMaxLeaf / 32;
+constexpr int kMaxLeaf = 1024;  // leaf size limit (candidates per lane: 16 up to 512, 32 above)
 
 __device__ __forceinline__ bool less_dj(double d1, int j1, double d2, int j2) {
   return d1 < d2 || (d1 == d2 && j1 < j2);  // neighbor_less (neighbors.hpp:30-33)
@@ -73,7 +72,7 @@ __device__ __forceinline__ double sqnorm_diff(const double* xa, const double* xb
   return res;
 }
 
-template <int D>
+template <int D, int kPerLane>
 __global__ void __launch_bounds__(kWarps * 32) ann_leaf_kernel(const double* __restrict__ coords, int32_t d,
                                                                int32_t kind, double inv2h2,
                                                                const int32_t* __restrict__ leaf_off,
@@ -122,6 +121,19 @@ __global__ void __launch_bounds__(kWarps * 32) ann_leaf_kernel(const double* __r
     if (lane < olen) {
       oj = tj[size_t(i) * kappa + lane];
       od = td[size_t(i) * kappa + lane];
+    }
+    if (olen == kappa) {
+      // a full list only changes for candidates that beat its last entry (merge_candidates keeps
+      // the kappa smallest): drop the rest, and skip the row when nothing survives
+      const int wj = __shfl_sync(0xffffffffu, oj, kappa - 1);
+      const double wd = __shfl_sync(0xffffffffu, od, kappa - 1);
+      bool any = false;
+#pragma unroll
+      for (int u = 0; u < kPerLane; ++u) {
+        if (cj[u] >= 0 && !less_dj(cd[u], cj[u], wd, wj)) cj[u] = -1;
+        any |= cj[u] >= 0;
+      }
+      if (!__any_sync(0xffffffffu, any)) continue;
     }
     int outn = 0;
     int my_j = -1;
@@ -227,7 +239,8 @@ int gofmm_ann_leaf_merge(int32_t n, int32_t d, const double* coords, int32_t kin
   cudaEventCreate(&ev[0]);
   cudaEventCreate(&ev[1]);
   cudaEventRecord(ev[0]);
-  auto launch = [&](auto kern) {
+  auto launch = [&](auto k16, auto k32) {
+    auto kern = maxleaf <= 512 ? k16 : k32;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     kern<<<unsigned(nleaves), kWarps * 32, smem>>>(static_cast<double*>(dc.p), d, kind, inv,
                                                    static_cast<int32_t*>(dlo.p), static_cast<int32_t*>(dli.p), kappa,
@@ -235,10 +248,10 @@ int gofmm_ann_leaf_merge(int32_t n, int32_t d, const double* coords, int32_t kin
                                                    static_cast<int32_t*>(dtl.p));
   };
   switch (d) {
-    case 3: launch(ann_leaf_kernel<3>); break;
-    case 6: launch(ann_leaf_kernel<6>); break;
-    case 8: launch(ann_leaf_kernel<8>); break;
-    default: launch(ann_leaf_kernel<0>); break;
+    case 3: launch(ann_leaf_kernel<3, 16>, ann_leaf_kernel<3, 32>); break;
+    case 6: launch(ann_leaf_kernel<6, 16>, ann_leaf_kernel<6, 32>); break;
+    case 8: launch(ann_leaf_kernel<8, 16>, ann_leaf_kernel<8, 32>); break;
+    default: launch(ann_leaf_kernel<0, 16>, ann_leaf_kernel<0, 32>); break;
   }
   cudaEventRecord(ev[1]);
   e = cudaGetLastError();

@@ -109,6 +109,9 @@ constexpr int kStagesGW = 3, kBM_GW = 32, kBN_GW = 512;
 #define CFG_GW kBM_GW, kBN_GW, 2, 8, kStagesGW
 #define CFG_GN64 kBM_G, 64, 4, 4, kStagesG
 #define CFG_GN128 kBM_G, 128, 4, 4, kStagesG
+// GN64W: 32-row tiles for r <= 64 — twice the CTAs and half the stage of GN64 for the
+// latency-bound upper levels (config 1: 16-64 groups per level, chains of up to 80 stages)
+#define CFG_GN64W kBM_GW, 64, 2, 8, kStagesG
 // SN64: stored operands for r <= 64 (64x64 tiles: twice the CTAs of S, no idle columns)
 #define CFG_SN64 kBM_G, 64, 4, 4, kStagesS
 constexpr int kBM[3] = {kBM_S, kBM_G, kBM_GW};  // tile-row classes of the FP64 tile lists
@@ -119,16 +122,18 @@ using KernelFn = void (*)(BMaps, const Tile*, const Group*, const Term*, int32_t
                           int32_t);
 
 struct GenKernel {
-  KernelFn fn, fn_wide, fn_n64, fn_n128;
-  size_t smem, smem_wide, smem_n64, smem_n128;
+  KernelFn fn, fn_wide, fn_n64, fn_n128, fn_n64w;
+  size_t smem, smem_wide, smem_n64, smem_n128, smem_n64w;
 };
 
 template <int KIND, int DIM>
 GenKernel gen_kernel() {
   return {&grouped_gemm_f64<CFG_G, KIND, DIM>,           &grouped_gemm_f64<CFG_GW, KIND, DIM>,
           &grouped_gemm_f64<CFG_GN64, KIND, DIM>,        &grouped_gemm_f64<CFG_GN128, KIND, DIM>,
+          &grouped_gemm_f64<CFG_GN64W, KIND, DIM>,
           gemm_smem_bytes<CFG_G, KIND, DIM>(),           gemm_smem_bytes<CFG_GW, KIND, DIM>(),
-          gemm_smem_bytes<CFG_GN64, KIND, DIM>(),        gemm_smem_bytes<CFG_GN128, KIND, DIM>()};
+          gemm_smem_bytes<CFG_GN64, KIND, DIM>(),        gemm_smem_bytes<CFG_GN128, KIND, DIM>(),
+          gemm_smem_bytes<CFG_GN64W, KIND, DIM>()};
 }
 
 // wide generated tiles (32 x 512) once the chunk has more than 256 columns
@@ -487,8 +492,8 @@ struct gofmm_handle {
   int32_t maps32_r = 0;
 
   gofmm::KernelFn kfn_s = nullptr, kfn_sn64 = nullptr, kfn_g = nullptr, kfn_gw = nullptr, kfn_gn64 = nullptr,
-                  kfn_gn128 = nullptr;
-  size_t smem_s = 0, smem_sn64 = 0, smem_g = 0, smem_gw = 0, smem_gn64 = 0, smem_gn128 = 0;
+                  kfn_gn128 = nullptr, kfn_gn64w = nullptr;
+  size_t smem_s = 0, smem_sn64 = 0, smem_g = 0, smem_gw = 0, smem_gn64 = 0, smem_gn128 = 0, smem_gn64w = 0;
   gofmm::BMaps maps_s{}, maps_g{}, maps_n64{};  // B boxes of 128 / 256 / 64 columns
   int32_t maps_r = 0;  // r the tensor maps were encoded for
   int64_t flops_per_rhs = 0;
@@ -1192,6 +1197,9 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     H->smem_gn64 = gk.smem_n64;
     H->kfn_gn128 = gk.fn_n128;
     H->smem_gn128 = gk.smem_n128;
+    H->kfn_gn64w = gk.fn_n64w;
+    H->smem_gn64w = gk.smem_n64w;
+    GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_gn64w, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_gn64w)));
     GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_gn64, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_gn64)));
     GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_gn128, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_gn128)));
     GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_g, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_g)));
@@ -1343,7 +1351,7 @@ LaunchCfg pick_launch_cfg(const gofmm_handle* H, const Launch& L, int32_t r) {
     int bm;
     double eff;  // achieved fraction of the DMMA peak when the SMs are full (measured, rounded)
   };
-  Cand c[4];
+  Cand c[5];
   int nc = 0;
   if (!L.gen) {
     if (r > 64) c[nc++] = {{H->kfn_s, H->smem_s, kBN_S, &H->maps_s, 0}, kBM_S, 0.80};
@@ -1353,6 +1361,7 @@ LaunchCfg pick_launch_cfg(const gofmm_handle* H, const Launch& L, int32_t r) {
     if (r > 128) c[nc++] = {{H->kfn_g, H->smem_g, kBN_G, &H->maps_g, 1}, kBM_G, 0.75};
     if (r > 64) c[nc++] = {{H->kfn_gn128, H->smem_gn128, 128, &H->maps_s, 1}, kBM_G, 0.65};
     c[nc++] = {{H->kfn_gn64, H->smem_gn64, 64, &H->maps_n64, 1}, kBM_G, 0.55};
+    c[nc++] = {{H->kfn_gn64w, H->smem_gn64w, 64, &H->maps_n64, 2}, kBM_GW, 0.40};
   }
   int best = 0;
   double best_t = 0.0;
