@@ -115,8 +115,7 @@ constexpr int kStagesGW = 3, kBM_GW = 32, kBN_GW = 512;
 // SN64: stored operands for r <= 64 (64x64 tiles: twice the CTAs of S, no idle columns)
 #define CFG_SN64 kBM_G, 64, 4, 4, kStagesS
 constexpr int kBM[3] = {kBM_S, kBM_G, kBM_GW};  // tile-row classes of the FP64 tile lists
-constexpr int kThreadsS = kProducerThreads + kConsumerThreads;
-constexpr int kThreadsG = kProducerThreads + kConsumerThreads;
+constexpr int kThreadsG = kProducerThreads + kConsumerThreads;  // every FP64 config: producer WG + 16 consumer warps
 
 using KernelFn = void (*)(BMaps, const Tile*, const Group*, const Term*, int32_t, KernelParams, double*, int64_t,
                           int32_t);
@@ -260,6 +259,7 @@ struct Launch {
 };
 
 constexpr int kOutParts = 4;
+static_assert(kOutParts <= 8, "per-part D2H timing events (gofmm_handle::dpev)");
 
 // the part boundaries of an output launch: groups split into kOutParts runs of leaves; valid only
 // if consecutive runs cover consecutive u_perm rows (leaves in left-to-right order)

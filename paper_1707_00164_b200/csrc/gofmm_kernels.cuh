@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
   const int m0 = tile.m0;
   const int n0 = blockIdx.y * BN;
   const int M = grp.M;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   const int dim = (DIM > 0) ? DIM : kp.dim;
 
   if (threadIdx.x == 0) {
