@@ -7,9 +7,9 @@
 // clamped to [1, s], skeleton = the first `rank` pivots, and proj = [I | R11^{-1} R12] scattered
 // back through the column permutation (the triangular solve of eigen_shim:605-625).
 //
-// One CTA per node. The node's block lives ROW-major in a global workspace so that every
-// per-column pass (one thread per column: Householder dot product, rank-1 update, norm
-// downdate) reads one coalesced row segment per step; per-step vectors (column norms, the
+// One CTA per node (3 per SM). The node's block lives ROW-major in a global workspace so that
+// every per-column pass (a thread per aligned column pair: Householder dot product, rank-1
+// update; a thread per column: norm downdate) reads coalesced row segments, 16 rows in flight; per-step vectors (column norms, the
 // Householder vector, tau * v) live in shared memory. Every floating-point operation is issued
 // with explicit round-to-nearest intrinsics in the reference's order (no FMA contraction, the
 // same 2- and 4-accumulator reduction trees), so pivots, ranks, skeletons and proj reproduce
@@ -28,7 +28,7 @@
 
 namespace gofmm_skel {
 
-constexpr int kThreads = 128;  // 4 CTAs (nodes) per SM: one node's serial pivot phase overlaps the others' streaming
+constexpr int kThreads = 128;  // 3 CTAs (nodes) per SM: one node's serial pivot phase overlaps the others' streaming
 
 struct NodeDesc {
   int64_t in_off;    // block (column-major rows x cols) in the input blob
@@ -123,7 +123,7 @@ __device__ double gemv_dot_col(int n, const double* __restrict__ col, int64_t ld
   return cc;
 }
 
-__global__ void __launch_bounds__(kThreads, 4) skeletonize_kernel(const NodeDesc* __restrict__ nodes,
+__global__ void __launch_bounds__(kThreads, 3) skeletonize_kernel(const NodeDesc* __restrict__ nodes,
                                                                const double* __restrict__ in, double* __restrict__ ws,
                                                                int32_t s_max, double tau_tol,
                                                                int32_t* __restrict__ rank_out,
@@ -273,12 +273,12 @@ __global__ void __launch_bounds__(kThreads, 4) skeletonize_kernel(const NodeDesc
         const double* b = &A[int64_t(k + 1) * ld + j0];
         double c0a = 0.0, c1a = 0.0, c0b = 0.0, c1b = 0.0;
         int i = 0;
-        for (; i + 8 <= m1; i += 8) {
-          double2 x[8];
+        for (; i + 16 <= m1; i += 16) {
+          double2 x[16];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) x[u] = *reinterpret_cast<const double2*>(b + int64_t(i + u) * ld);
+          for (int u = 0; u < 16; ++u) x[u] = *reinterpret_cast<const double2*>(b + int64_t(i + u) * ld);
 #pragma unroll
-          for (int u = 0; u < 8; u += 2) {
+          for (int u = 0; u < 16; u += 2) {
             c0a = add(c0a, mul(x[u].x, ess[i + u]));
             c1a = add(c1a, mul(x[u + 1].x, ess[i + u + 1]));
             c0b = add(c0b, mul(x[u].y, ess[i + u]));
@@ -310,8 +310,21 @@ __global__ void __launch_bounds__(kThreads, 4) skeletonize_kernel(const NodeDesc
         }
         double* bw = &A[int64_t(k + 1) * ld + j0];
         if (act0 && act1) {
-#pragma unroll 8
-          for (int r = 0; r < m1; ++r) {
+          // rows in blocks of 8: all loads of a block are issued before its stores (the compiler
+          // cannot reorder loads across stores through the runtime stride on its own)
+          int r = 0;
+          for (; r + 16 <= m1; r += 16) {
+            double2 v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = *reinterpret_cast<const double2*>(bw + int64_t(r + u) * ld);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              v[u].x = sub(v[u].x, mul(ta, tess[r + u]));
+              v[u].y = sub(v[u].y, mul(tb, tess[r + u]));
+              *reinterpret_cast<double2*>(bw + int64_t(r + u) * ld) = v[u];
+            }
+          }
+          for (; r < m1; ++r) {
             double2 v = *reinterpret_cast<double2*>(bw + int64_t(r) * ld);
             v.x = sub(v.x, mul(ta, tess[r]));
             v.y = sub(v.y, mul(tb, tess[r]));
@@ -320,8 +333,15 @@ __global__ void __launch_bounds__(kThreads, 4) skeletonize_kernel(const NodeDesc
         } else {
           double* c = bw + (act0 ? 0 : 1);
           const double t = act0 ? ta : tb;
-#pragma unroll 8
-          for (int r = 0; r < m1; ++r) c[int64_t(r) * ld] = sub(c[int64_t(r) * ld], mul(t, tess[r]));
+          int r = 0;
+          for (; r + 8 <= m1; r += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = c[int64_t(r + u) * ld];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) c[int64_t(r + u) * ld] = sub(v[u], mul(t, tess[r + u]));
+          }
+          for (; r < m1; ++r) c[int64_t(r) * ld] = sub(c[int64_t(r) * ld], mul(t, tess[r]));
         }
       }
     }

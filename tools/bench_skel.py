@@ -25,7 +25,7 @@ def gaussian_block(rng, rows, cols, d, h=1.0):
 
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--nodes", type=int, default=592)
+ap.add_argument("--nodes", type=int, default=1776)
 ap.add_argument("--rows", type=int, default=1056)
 ap.add_argument("--cols", type=int, default=1024)
 ap.add_argument("--cpu-nodes", type=int, default=16)
