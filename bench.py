@@ -438,6 +438,29 @@ def dist_arm(args, world, rank, local):
     value = full_flops / (ms * 1e-3) / 1e9
     peak, peak_src = tf32x3_peak_tflops() if f32 else fp64_peak_tflops()
 
+    # zero-communication baseline: the whole tree replicated on every GPU, each
+    # evaluating r / N of the columns (evaluation is column-separable)
+    rhs_shard = None
+    if world > 1 or args.rhs_shard:
+        rl = max(1, r // world)
+        ev1 = Evaluator(tree, device=local, precision=args.precision)
+        w1, u1 = w[:, :rl], torch.empty((rl, tree.n), dtype=tdt, device="cuda").t()
+        ev1.evaluate_torch(w1, out=u1)
+        torch.cuda.synchronize()
+        barrier(world)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            ev1.evaluate_torch(w1, out=u1)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ms1 = allmax(f0.elapsed_time(f1) / args.steps, world)
+        rhs_shard = {"value": round(world * ev1.flops(rl) / (ms1 * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+                     "ms_per_step": round(ms1, 3), "r_per_gpu": rl,
+                     "note": "zero-communication baseline: replicated tree, r/N columns per GPU"}
+        ev1.close()
+        del w1, u1
+
     # end to end: pinned host W -> device, evaluation, own rows of u -> pinned host
     e2e = None
     if not args.no_e2e:
@@ -475,8 +498,15 @@ def dist_arm(args, world, rank, local):
         "flops_per_eval": int(full_flops),
         "rank_flops_max": int(allmax(float(info["flops_per_rhs"] * r), world)),
         "rel_error": None,
-        "roofline": None,
+        # whole rank step (the distributed stages do not time single launches): the busiest
+        # rank's reference-counted flops over the step time, against one GPU's peak
+        "roofline": {"bound": "tensor", "kernel": "whole subtree-split step (busiest rank)",
+                     "achieved": round(allmax(float(info["flops_per_rhs"] * r), world) / (ms * 1e-3) / 1e12, 3),
+                     "peak": peak, "unit": "TFLOP/s",
+                     "frac": round(allmax(float(info["flops_per_rhs"] * r), world) / (ms * 1e-3) / 1e12 / peak, 4),
+                     "traffic": None, "peak_source": peak_src},
         "cpu_baseline": None,
+        "rhs_shard_baseline": rhs_shard,
         "e2e": e2e,
         "gpu_launches": int((ev.launches_per_eval + 2) * args.steps),
         "setup_s": {"tree_gen": round(t_gen, 2), "create_upload": round(t_create, 2)},
@@ -505,6 +535,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dist", action="store_true", help="use the subtree-split path even on one GPU")
+    ap.add_argument("--rhs-shard", action="store_true",
+                    help="also time the zero-communication RHS-sharding baseline on one GPU (always on for N > 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     world, rank, local = dist_setup()
