@@ -335,6 +335,10 @@ struct DistPlan {
 
 inline int64_t pad16_(int64_t x) { return (x + 15) & ~int64_t(15); }
 
+// levels below log2(P) the subtree split may go for load balance (more, smaller subtrees per rank;
+// everything above the split is replicated on every rank)
+constexpr int kSplitExtra = 3;
+
 DistPlan make_dist_plan(int nranks, int nn, const int32_t* left, const int32_t* right, const int32_t* level,
                         const int32_t* start, const int32_t* end, const int32_t* rank, int64_t n_near,
                         const int32_t* near_a, const int32_t* near_b, int64_t n_far, const int32_t* far_a,
@@ -345,21 +349,78 @@ DistPlan make_dist_plan(int nranks, int nn, const int32_t* left, const int32_t* 
     throw Error(GOFMM_ERR_INVALID, "the number of ranks must be a power of two");
   int l = 0;
   while ((1 << l) < nranks) ++l;
-  P.split = l;
   // every node above the split must be interior so that level l has exactly nranks nodes
-  std::vector<int> at_split;
-  for (int i = 0; i < nn; ++i) {
-    if (level[i] < l && left[i] < 0)
-      throw Error(GOFMM_ERR_INVALID, "tree too shallow for " + std::to_string(nranks) + " ranks");
-    if (level[i] == l) at_split.push_back(i);
-  }
-  if (int(at_split.size()) != nranks) throw Error(GOFMM_ERR_INVALID, "split level does not have one node per rank");
-  P.owner.assign(nn, -1);
-  for (int g = 0; g < nranks; ++g) P.owner[at_split[g]] = g;
-  for (int i = 0; i < nn; ++i)  // BFS order: parents first
-    if (level[i] >= l && left[i] >= 0) P.owner[left[i]] = P.owner[right[i]] = P.owner[i];
+  int min_leaf_level = 1 << 30;
   for (int i = 0; i < nn; ++i)
-    if (level[i] > l && P.owner[i] < 0) {
+    if (left[i] < 0) min_leaf_level = std::min(min_leaf_level, int(level[i]));
+  if (min_leaf_level < l) throw Error(GOFMM_ERR_INVALID, "tree too shallow for " + std::to_string(nranks) + " ranks");
+  // Load balance: the split goes up to kSplitExtra levels deeper than log2(P) (tree permitting),
+  // and each rank owns a CONTIGUOUS run of those subtrees (left to right, so its rows stay one
+  // range) chosen to minimise the largest per-rank work. The work of a subtree is the reference
+  // flop counter of the tasks whose output it owns (evaluate.hpp:154-214, per RHS column).
+  const int extra = nranks > 1 ? std::min(kSplitExtra, min_leaf_level - l) : 0;
+  const int ls = l + extra;
+  P.split = ls;
+  std::vector<int> at_split;
+  for (int i = 0; i < nn; ++i)
+    if (level[i] == ls) at_split.push_back(i);
+  std::sort(at_split.begin(), at_split.end(), [&](int x, int y) { return start[x] < start[y]; });
+  if (int(at_split.size()) != (1 << ls)) throw Error(GOFMM_ERR_INVALID, "split level is not a complete tree level");
+  std::vector<double> work(nn, 0.0);
+  {
+    std::vector<int32_t> par(nn, -1);
+    for (int i = 0; i < nn; ++i)
+      if (left[i] >= 0) par[left[i]] = par[right[i]] = i;
+    auto npts = [&](int i) { return double(end[i] - start[i]); };
+    for (int i = 0; i < nn; ++i) {
+      const double k = rank[i] >= 0 ? double(rank[i]) : 0.0;
+      if (left[i] < 0) {
+        work[i] += 2.0 * npts(i) * npts(i) + 2.0 * k * npts(i) + 2.0 * k * npts(i);  // D, leaf S2N, N2S
+      } else if (rank[i] >= 0) {
+        const double c = double(std::max(rank[left[i]], 0) + std::max(rank[right[i]], 0));
+        work[i] += 2.0 * k * c;  // N2S
+      }
+      if (par[i] >= 0 && rank[par[i]] >= 0 && rank[i] >= 0) work[i] += 2.0 * rank[par[i]] * k;  // S2N
+    }
+    for (int64_t t = 0; t < n_far; ++t) {
+      const double f = 2.0 * std::max(rank[far_a[t]], 0) * std::max(rank[far_b[t]], 0);
+      work[far_a[t]] += f;
+      work[far_b[t]] += f;
+    }
+    for (int64_t t = 0; t < n_near; ++t) {
+      const double f = 2.0 * npts(near_a[t]) * npts(near_b[t]);
+      work[near_a[t]] += f;
+      work[near_b[t]] += f;
+    }
+    for (int i = nn - 1; i >= 0; --i)  // BFS ids: children after parents
+      if (left[i] >= 0 && level[i] >= ls) work[i] += work[left[i]] + work[right[i]];
+  }
+  // optimal contiguous partition of the S subtrees into nranks runs (min over max run work)
+  const int S = int(at_split.size());
+  std::vector<double> pre(S + 1, 0.0);
+  for (int t = 0; t < S; ++t) pre[t + 1] = pre[t] + work[at_split[t]];
+  std::vector<std::vector<double>> best(nranks + 1, std::vector<double>(S + 1, 1e300));
+  std::vector<std::vector<int>> cut(nranks + 1, std::vector<int>(S + 1, 0));
+  best[0][0] = 0.0;
+  for (int g = 1; g <= nranks; ++g)
+    for (int e = g; e <= S; ++e)
+      for (int b = g - 1; b < e; ++b) {
+        const double v = std::max(best[g - 1][b], pre[e] - pre[b]);
+        if (v < best[g][e]) {
+          best[g][e] = v;
+          cut[g][e] = b;
+        }
+      }
+  P.owner.assign(nn, -1);
+  for (int g = nranks, e = S; g >= 1; --g) {
+    const int b = cut[g][e];
+    for (int t = b; t < e; ++t) P.owner[at_split[t]] = g - 1;
+    e = b;
+  }
+  for (int i = 0; i < nn; ++i)  // BFS order: parents first
+    if (level[i] >= ls && left[i] >= 0) P.owner[left[i]] = P.owner[right[i]] = P.owner[i];
+  for (int i = 0; i < nn; ++i)
+    if (level[i] > ls && P.owner[i] < 0) {
       // children were assigned from their parent above; a node deeper than l with no owner
       // would mean an inconsistent tree
       throw Error(GOFMM_ERR_INVALID, "node below the split without an owning subtree");

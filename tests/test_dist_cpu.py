@@ -1,5 +1,6 @@
 """Multi-process CPU test (gloo, world_size 2 and 4) of the subtree-split host logic
-(north_star (4)): every rank plans its part with gofmm_dist_plan_host (no device);
+(north_star (4)): every rank plans its part with gofmm_dist_plan_host (no device):
+a work-balanced contiguous run of the subtrees up to two levels below log2(P);
 the ranks all-gather their plans and check, against an independent Python restatement, that
 (1) the owned row ranges partition [0, N); (2) every ghost a rank needs (what of cross-subtree
 far partners and of all split-level nodes, W rows of cross-subtree near partners) is exported by
@@ -23,14 +24,15 @@ def _free_port():
     return p
 
 
-def independent_needs(t, rank, nranks):
-    """Python restatement of what `rank` needs from other ranks."""
-    l = int(np.log2(nranks))
+def independent_needs(t, rank, split_level, ranges):
+    """Python restatement of what `rank` needs from other ranks, given the plan's split level and
+    every rank's owned row range (each rank owns the split-level subtrees inside its range)."""
+    l = split_level
     nn = t.num_nodes
     owner = np.full(nn, -1)
     split = [i for i in range(nn) if t.level[i] == l]
-    for g, i in enumerate(split):
-        owner[i] = g
+    for i in split:
+        owner[i] = next(g for g, (b, e) in enumerate(ranges) if b <= t.start[i] < e)
     for i in range(nn):
         if t.level[i] >= l and t.left[i] >= 0:
             owner[t.left[i]] = owner[t.right[i]] = owner[i]
@@ -57,7 +59,9 @@ def _worker(rank, world, port, q):
         info, ids = gofmm.dist_plan_host(tree, rank, world)
         plans = [None] * world
         dist.all_gather_object(plans, (info, ids))
-        owner, need_what, need_w = independent_needs(tree, rank, world)
+        ranges_by_rank = [(p[0]["own_row_begin"], p[0]["own_row_end"]) for p in plans]
+        assert len({p[0]["split_level"] for p in plans}) == 1
+        owner, need_what, need_w = independent_needs(tree, rank, info["split_level"], ranges_by_rank)
         exported_what, exported_w = set(), set()
         for h, (inf, exp) in enumerate(plans):
             if h == rank:
@@ -71,7 +75,8 @@ def _worker(rank, world, port, q):
         assert ranges[0][0] == 0 and ranges[-1][1] == tree.n
         assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
         own_split = [i for i in range(tree.num_nodes) if owner[i] == rank and tree.level[i] == info["split_level"]]
-        assert len(own_split) == 1
+        assert len(own_split) >= 1  # a contiguous run of split-level subtrees (load balance)
+        assert info["split_level"] >= int(np.log2(world))
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))
