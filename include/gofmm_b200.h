@@ -175,10 +175,11 @@ typedef struct gofmm_launch_info {
 int gofmm_launch_profile(const gofmm_handle* h, int32_t r, int32_t cap, gofmm_launch_info* out, int32_t* count);
 
 /* ---- multi-GPU: subtree split (north_star (4)) ------------------------------
- * nranks = 2^l GPUs; the tree is split at level l, rank g owns the g-th level-l subtree
- * (permuted rows [own_row_begin, own_row_end)); nodes above level l are evaluated redundantly.
+ * nranks = 2^l GPUs; the tree is split at level s = l + up to 3 (split_level), and rank g owns a
+ * contiguous, work-balanced run of the level-s subtrees (permuted rows [own_row_begin,
+ * own_row_end)); nodes above level s are evaluated redundantly on every rank.
  * One all-gather per evaluation: stage1 packs this rank's exports (the skeleton weights `what`
- * other ranks need — all level-l nodes plus cross-subtree far-field partners — and the W rows
+ * other ranks need — all level-s nodes plus cross-subtree far-field partners — and the W rows
  * of leaves that are cross-subtree near-field partners) into a send buffer of
  * max_send_rows x r doubles; the caller all-gathers the nranks send buffers (e.g. ncclAllGather
  * via torch.distributed) into recv (nranks * max_send_rows * r doubles, rank order); stage2

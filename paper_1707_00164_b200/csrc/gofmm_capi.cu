@@ -313,10 +313,11 @@ void order_longest_first(std::vector<Tile>& tiles, int b, int e, const GroupVec&
 }
 
 // ---------------------------------------------------------------- subtree-split distribution
-// north_star (4): for P = 2^l GPUs the tree is split at level l into P subtrees, one per rank.
-// Rank g owns the nodes below its level-l node; nodes above level l ("top") are evaluated
-// redundantly by every rank. One all-gather per evaluation exchanges, from every rank, the
-// skeleton weights (what) other ranks need (all level-l nodes for the top N2S, plus far-field
+// north_star (4): for P = 2^l GPUs the tree is split into subtrees at level s = l + up to
+// kSplitExtra, and rank g owns a contiguous, work-balanced run of them (make_dist_plan); nodes
+// above level s ("top") are evaluated redundantly by every rank. One all-gather per evaluation
+// exchanges, from every rank, the skeleton weights (what) other ranks need (all level-s nodes
+// for the top N2S, plus far-field
 // partners across subtrees) and the W rows of leaves that are near-field partners across
 // subtrees. Everything below is pure host logic over the flattened tree.
 struct Seg {
@@ -349,7 +350,7 @@ DistPlan make_dist_plan(int nranks, int nn, const int32_t* left, const int32_t* 
     throw Error(GOFMM_ERR_INVALID, "the number of ranks must be a power of two");
   int l = 0;
   while ((1 << l) < nranks) ++l;
-  // every node above the split must be interior so that level l has exactly nranks nodes
+  // every node above the split must be interior (no leaf above level l)
   int min_leaf_level = 1 << 30;
   for (int i = 0; i < nn; ++i)
     if (left[i] < 0) min_leaf_level = std::min(min_leaf_level, int(level[i]));
