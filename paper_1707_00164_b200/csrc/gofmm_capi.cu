@@ -118,7 +118,7 @@ constexpr int kBM[3] = {kBM_S, kBM_G, kBM_GW};  // tile-row classes of the FP64 
 constexpr int kThreadsG = kProducerThreads + kConsumerThreads;  // every FP64 config: producer WG + 16 consumer warps
 
 using KernelFn = void (*)(BMaps, const Tile*, const Group*, const Term*, int32_t, KernelParams, double*, int64_t,
-                          int32_t);
+                          int32_t, int32_t);
 
 struct GenKernel {
   KernelFn fn, fn_wide, fn_n64, fn_n128, fn_n64w;
@@ -496,6 +496,8 @@ struct gofmm_handle {
   cudaEvent_t pev[2][4] = {};
   cudaEvent_t tev[2][4] = {};
   cudaEvent_t dpev[8][2] = {};  // per-part D2H timing of a split output launch (<= kOutParts)
+  cudaEvent_t hpev[8] = {};     // column pieces of a single-chunk upload landed (H2D / N2S overlap)
+  cudaEvent_t upev[2] = {};     // upward phase of a piece-pipelined evaluation (timing)
   gofmm::DevBuf d_win2[2], d_uout2[2];
   std::vector<cudaEvent_t> lev;  // per-launch start/stop events (timed evaluations only)
   std::vector<float> launch_ms;  // durations of the last timed evaluation (summed over chunks)
@@ -1443,9 +1445,14 @@ LaunchCfg pick_launch_cfg(const gofmm_handle* H, const Launch& L, int32_t r) {
 // launch is enqueued, with the u_perm rows that part completes; returns whether it was used.
 using RowsDone = std::function<void(int64_t row0, int64_t row1)>;
 
+// Column pieces (host-buffer pipeline, stage 0): with c1 >= 0 only the permutation and the upward
+// (N2S) launches run, for columns [c0, c1) — N2S is column-separable, so a piece can start as
+// soon as its W columns have landed; phase_lo = 1 then runs the rest without the permutation.
 void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double* d_u, int64_t ldu,
                    cudaStream_t st, bool timed, int stage = 0, double* d_xbuf = nullptr,
-                   const RowsDone* rows_done = nullptr, bool* rows_used = nullptr) {
+                   const RowsDone* rows_done = nullptr, bool* rows_used = nullptr, int phase_lo = 0,
+                   int32_t c0 = 0, int32_t c1 = -1) {
+  const bool piece = c1 >= 0;
   ensure_workspace(H, r);
   upload_plan(H);
   encode_maps(H, r);
@@ -1456,16 +1463,17 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
     panel_copy<<<grid, 256, 0, st>>>(H->d_segs.as<PanelSeg>() + H->n_pack, H->d_what.as<double>(),
                                      H->d_wp.as<double>(), int64_t(H->ws_r) * 16, d_xbuf, r, 0);
   }
-  if (stage != 2) {
+  if (stage != 2 && phase_lo == 0) {
     // K5: row gather into the padded leaf layout (evaluate.hpp:294-295). Blocks walk all rows of
     // cpb columns before the next columns (grid.x = rows), so the randomly gathered source
     // columns (N * cpb * 8 bytes) stay L2-resident: each 32-byte sector is fetched from HBM once.
     const int cpb = int(std::max<int64_t>(1, std::min<int64_t>(8, (48ll << 20) / (int64_t(H->n) * 8))));
     const int64_t row0 = stage == 1 ? H->own_pst_begin : 0, row1 = stage == 1 ? H->own_pst_end : H->ld_wp;
-    if (row1 > row0) {
-      dim3 grid(unsigned((row1 - row0 + 255) / 256), unsigned((r + cpb - 1) / cpb));
-      permute_rows_in<<<grid, 256, 0, st>>>(d_w, ldw, H->d_prow.as<int32_t>(), row0, row1, r, cpb,
-                                            H->d_wp.as<double>(), int64_t(H->ws_r) * 16);
+    const int32_t pc0 = piece ? c0 : 0, pr = piece ? c1 - c0 : r;  // columns of this piece
+    if (row1 > row0 && pr > 0) {
+      dim3 grid(unsigned((row1 - row0 + 255) / 256), unsigned((pr + cpb - 1) / cpb));
+      permute_rows_in<<<grid, 256, 0, st>>>(d_w + size_t(pc0) * ldw, ldw, H->d_prow.as<int32_t>(), row0, row1, pr,
+                                            cpb, H->d_wp.as<double>() + 16 * size_t(pc0), int64_t(H->ws_r) * 16);
     }
   }
   // ev[1 + p] marks the start of phase p (0 upward, 1 downward, 2 output); ev[4] the end
@@ -1473,6 +1481,15 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
   int marked = 1;
   for (const Launch& L : H->launches) {
     if (stage != 0 && L.stage != stage) continue;
+    if (piece && L.phase != 0) continue;
+    if (L.phase < phase_lo) {  // ran in the column pieces: zero-length timing pair
+      const size_t li = size_t(&L - H->launches.data());
+      if (timed) {
+        GOFMM_CUDA(cudaEventRecord(H->lev[2 * li], st));
+        GOFMM_CUDA(cudaEventRecord(H->lev[2 * li + 1], st));
+      }
+      continue;
+    }
     while (timed && marked <= L.phase) GOFMM_CUDA(cudaEventRecord(H->ev[1 + marked++], st));
     double* cbase;
     int64_t ldc;
@@ -1485,11 +1502,12 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
     const size_t li = size_t(&L - H->launches.data());
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li], st));
     const LaunchCfg cfg = pick_launch_cfg(H, L, r);
+    const int32_t n_off = piece ? c0 : 0, ncols = piece ? c1 - c0 : r;
     auto run = [&](int t0, int nt) {
-      if (nt <= 0) return;
-      dim3 grid(unsigned(nt), unsigned((r + cfg.bn - 1) / cfg.bn));
+      if (nt <= 0 || ncols <= 0) return;
+      dim3 grid(unsigned(nt), unsigned((ncols + cfg.bn - 1) / cfg.bn));
       cfg.fn<<<grid, kThreadsG, cfg.smem, st>>>(*cfg.maps, H->d_tiles.as<Tile>() + t0, H->d_groups.as<Group>(),
-                                                 H->d_terms.as<Term>(), r, H->kp, cbase, ldc, cpanel);
+                                                 H->d_terms.as<Term>(), r, H->kp, cbase, ldc, cpanel, n_off);
     };
     if (rows_done && stage == 0 && L.out == Buf::Out && !L.parts.empty()) {
       for (size_t p = 0; p + 1 < L.parts.size(); ++p) {
@@ -1962,6 +1980,10 @@ int gofmm_destroy(gofmm_handle* H) {
     for (auto& row : H->dpev)
       for (auto& e : row)
         if (e) cudaEventDestroy(e);
+    for (auto& e : H->hpev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : H->upev)
+      if (e) cudaEventDestroy(e);
     if (H->gexec) cudaGraphExecDestroy(H->gexec);
     if (H->cap_stream) cudaStreamDestroy(H->cap_stream);
     delete H;
@@ -2059,6 +2081,8 @@ void evaluate_host(gofmm_handle* H, const T* w, int64_t ldw, int32_t r, T* u_per
       for (auto& e : row) GOFMM_CUDA(cudaEventCreate(&e));
     for (auto& row : H->dpev)
       for (auto& e : row) GOFMM_CUDA(cudaEventCreate(&e));
+    for (auto& e : H->hpev) GOFMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : H->upev) GOFMM_CUDA(cudaEventCreate(&e));
   }
   // chunk: one N tile of the generated-operand kernels (FP32: 256 columns; FP64: 512 columns,
   // the GW config, once r > 256) unless r is smaller or the workspace forces less
@@ -2100,14 +2124,32 @@ void evaluate_host(gofmm_handle* H, const T* w, int64_t ldw, int32_t r, T* u_per
     if (stats) GOFMM_CUDA(cudaEventRecord(H->tev[b][1], H->s_h2d));
     GOFMM_CUDA(cudaEventRecord(H->pev[b][0], H->s_h2d));  // in_ready
   };
-  if (nchunks > 0) h2d_copy(0);
+  // FP64 single chunk: W lands in column pieces and each piece's permutation + upward (N2S,
+  // column-separable) starts as soon as it is in HBM, so the upload overlaps the upward pass
+  constexpr int32_t kPieceCols = 128;
+  const int npieces = (!kF32 && nchunks == 1 && rc > kPieceCols) ? int((rc + kPieceCols - 1) / kPieceCols) : 0;
+  if (npieces > 8) throw Error(GOFMM_ERR_CUDA, "internal: too many column pieces");
+  if (npieces > 0) {
+    if (stats) GOFMM_CUDA(cudaEventRecord(H->tev[0][0], H->s_h2d));
+    for (int p = 0; p < npieces; ++p) {
+      const int32_t p0 = p * kPieceCols, pn = std::min(kPieceCols, rc - p0);
+      GOFMM_CUDA(cudaMemcpy2DAsync(static_cast<T*>(H->d_win2[0].p) + size_t(p0) * H->n, per_col,
+                                   w + size_t(p0) * ldw, size_t(ldw) * sizeof(T), per_col, pn,
+                                   cudaMemcpyHostToDevice, H->s_h2d));
+      GOFMM_CUDA(cudaEventRecord(H->hpev[p], H->s_h2d));
+    }
+    if (stats) GOFMM_CUDA(cudaEventRecord(H->tev[0][1], H->s_h2d));
+    GOFMM_CUDA(cudaEventRecord(H->pev[0][0], H->s_h2d));
+  } else if (nchunks > 0) {
+    h2d_copy(0);
+  }
   int parts_timed = 0;      // last chunk: D2H copies timed per part
   bool last_full = false;   // last chunk: whole-buffer D2H (no split) timed by tev
   for (int i = 0; i < nchunks; ++i) {
     const int b = i & 1;
     const int32_t c0 = i * rc, rr = std::min(rc, r - c0);
     if (i + 1 < nchunks) h2d_copy(i + 1);  // prefetch the next chunk before evaluating this one
-    GOFMM_CUDA(cudaStreamWaitEvent(st, H->pev[b][0], 0));            // W chunk landed
+    if (npieces == 0) GOFMM_CUDA(cudaStreamWaitEvent(st, H->pev[b][0], 0));  // W chunk landed (else per piece)
     if (i >= 2) GOFMM_CUDA(cudaStreamWaitEvent(st, H->pev[b][2], 0));  // u buffer downloaded
     // last chunk: its u rows are downloaded part by part behind the split output launch
     // (rows_done), so only the last part's download is exposed
@@ -2129,12 +2171,34 @@ void evaluate_host(gofmm_handle* H, const T* w, int64_t ldw, int32_t r, T* u_per
       rows_hi = std::max(rows_hi, r1);
     };
     const RowsDone* hook = (i + 1 == nchunks) ? &rows_done : nullptr;
-    if constexpr (kF32)
+    if constexpr (kF32) {
       enqueue32(H, H->d_win2[b].as<float>(), H->n, rr, H->d_uout2[b].as<float>(), H->n, st, stats != nullptr, hook,
                 &rows_used);
-    else
+    } else if (npieces > 0) {
+      double* dw = H->d_win2[b].as<double>();
+      double* du = H->d_uout2[b].as<double>();
+      if (stats) {
+        H->launch_ms.assign(H->launches.size(), 0.f);
+        std::fill(std::begin(H->phase_ms), std::end(H->phase_ms), 0.f);
+        GOFMM_CUDA(cudaEventRecord(H->upev[0], st));
+      }
+      for (int p = 0; p < npieces; ++p) {
+        GOFMM_CUDA(cudaStreamWaitEvent(st, H->hpev[p], 0));
+        const int32_t p0 = p * kPieceCols, p1 = std::min(rr, p0 + kPieceCols);
+        enqueue_chunk(H, dw, H->n, rr, du, H->n, st, false, 0, nullptr, nullptr, nullptr, 0, p0, p1);
+      }
+      if (stats) GOFMM_CUDA(cudaEventRecord(H->upev[1], st));
+      enqueue_chunk(H, dw, H->n, rr, du, H->n, st, stats != nullptr, 0, nullptr, hook, &rows_used, /*phase_lo=*/1);
+      if (stats) {
+        accumulate_chunk_times(H);
+        float up = 0.f;  // permutation + upward of all pieces, including waits for the upload
+        GOFMM_CUDA(cudaEventElapsedTime(&up, H->upev[0], H->upev[1]));
+        H->phase_ms[1] += up;  // [0] permutation, [1] upward (here: both, over all pieces)
+      }
+    } else {
       enqueue(H, H->d_win2[b].as<double>(), H->n, rr, H->d_uout2[b].as<double>(), H->n, st, stats != nullptr, hook,
               &rows_used);
+    }
     GOFMM_CUDA(cudaEventRecord(H->pev[b][1], st));  // comp_done: W buffer free, u chunk ready
     GOFMM_CUDA(cudaStreamWaitEvent(H->s_d2h, H->pev[b][1], 0));
     const bool split = rows_used && rows_lo == 0 && rows_hi == H->n;
@@ -2300,7 +2364,7 @@ int gofmm_exact_rows(gofmm_handle* H, const int32_t* rows, int32_t nrows, const 
     dim3 grid(unsigned(tl.size()), unsigned((r + kBN_G - 1) / kBN_G));
     H->kfn_g<<<grid, kThreadsG, H->smem_g, st>>>(H->maps_g, H->d_ex_tiles.as<Tile>(), H->d_ex_groups.as<Group>(),
                                                   H->d_ex_terms.as<Term>(), r, H->kp, H->d_ex_part.as<double>(), ldp,
-                                                  0);
+                                                  0, 0);
     dim3 g2(unsigned((int64_t(nrows) * r + 255) / 256));
     sum_partials<<<g2, 256, 0, st>>>(H->d_ex_part.as<double>(), ldp, nrows, chunks, r, d_out, ldo);
     GOFMM_CUDA(cudaGetLastError());

@@ -343,7 +343,7 @@ template <int BM, int BN, int WM, int WN, int STAGES, int KIND, int DIM>
 __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
     grouped_gemm_f64(const __grid_constant__ BMaps maps, const Tile* __restrict__ tiles,
                      const Group* __restrict__ groups, const Term* __restrict__ terms, int32_t R, KernelParams kp,
-                     double* __restrict__ cbase, int64_t ldc, int32_t cpanel) {
+                     double* __restrict__ cbase, int64_t ldc, int32_t cpanel, int32_t n_off) {
   constexpr bool kGen = (KIND != kKindNone);
   constexpr int XD = kGen ? (DIM > 0 ? DIM + 1 : kMaxDimRt + 1) : 0;  // odd stride: no bank conflicts
   constexpr int DD = DIM > 0 ? DIM : kMaxDimRt;
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
   const Tile tile = tiles[blockIdx.x];
   const Group grp = groups[tile.group];
   const int m0 = tile.m0;
-  const int n0 = blockIdx.y * BN;
+  const int n0 = n_off + blockIdx.y * BN;  // n_off: first column of a column-piece launch
   const int M = grp.M;
   const int lane = threadIdx.x & 31;
   const int dim = (DIM > 0) ? DIM : kp.dim;

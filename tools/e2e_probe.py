@@ -26,4 +26,5 @@ with Evaluator(tree, precision=prec) as ev:
         t1 = time.perf_counter()
         st = p.stats
         print(f"{cfg} {prec} call {i}: wall {1e3 * (t1 - t0):8.2f} ms  C {1e3 * st['seconds']:8.2f} ms  h2d {st['ms_h2d']:7.2f}"
-              f"  d2h {st['ms_d2h']:7.2f}  dev {st['ms_permute'] + st['ms_upward'] + st['ms_downward'] + st['ms_output']:8.2f}")
+              f"  d2h {st['ms_d2h']:7.2f}  dev {st['ms_permute'] + st['ms_upward'] + st['ms_downward'] + st['ms_output']:8.2f}"
+              f"  [perm {st['ms_permute']:.1f} up {st['ms_upward']:.1f} down {st['ms_downward']:.1f} out {st['ms_output']:.1f}]")
