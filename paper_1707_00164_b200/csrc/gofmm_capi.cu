@@ -247,6 +247,7 @@ struct Launch {
   int64_t flops_per_rhs = 0;  // reference-counted flops of this launch per RHS column
   int stage = 2;  // distributed evaluation: 1 = before the all-gather (own-subtree N2S), 2 = after
   int first_group = 0, ngroups = 0;      // groups [first_group, first_group + ngroups)
+  int reduce_first = 0, reduce_n = 0;    // split-chain reductions after this launch (chain_reduce)
   int first_tile32 = 0, ntiles32 = 0;    // FP32 plan: 128-row tiles of the same groups
   // output launch of a host-buffer evaluation: split into row-contiguous parts so the D2H of a
   // part's u rows overlaps the next part's kernel. parts[p] = first tile of part p in each tile
@@ -523,6 +524,10 @@ struct gofmm_handle {
   std::vector<gofmm::Launch> launches;
   std::vector<gofmm::Tile> tiles;
   gofmm::DevBuf d_tiles, d_groups, d_terms;
+  std::vector<gofmm::ChainReduce> reduces;  // split term chains (FP64 downward levels)
+  std::vector<int64_t> reduce_src;
+  gofmm::DevBuf d_reduces, d_reduce_src;
+  int64_t scratch_rows = 0;  // skeleton-space rows appended after the nodes for split segments
   bool plan_uploaded = false;
   int32_t plan_r = 0;  // workspace r the device term pointers were built for
 
@@ -1159,7 +1164,67 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
       }
       gs.push_back(std::move(g));
     }
+    // Latency-bound levels (few groups, long far-field chains — the upper levels; config 1 has
+    // chains of 80 k-stages on 16-64 groups): split a chain that is much longer than the level's
+    // per-SM share into segments of about that share. Segment 0 accumulates into the group's own
+    // rows, the others into scratch rows appended to skeleton space; chain_reduce adds them in
+    // segment order after the launch. FP64 only (the FP32 epilogue stores hi/lo operands).
+    const int first_reduce = int(H->reduces.size());
+    if (H->precision == GOFMM_PRECISION_F64 && !gs.empty()) {
+      auto stages = [](const HostTerm& t) { return int64_t((t.K + 15) / 16); };
+      int64_t sum = 0, mx = 0;
+      for (const HostGroup& g : gs) {
+        int64_t ch = 0;
+        for (const HostTerm& t : g.terms) ch += stages(t);
+        sum += ch * ((std::max(g.M, 0) + kBM_G - 1) / kBM_G);
+        mx = std::max(mx, ch);
+      }
+      const double fair = double(sum) / double(H->num_sms);
+      if (double(mx) > 2.0 * fair && mx >= 24) {
+        const int64_t target = std::max<int64_t>(8, int64_t(std::ceil(fair)));
+        std::vector<HostGroup> out;
+        for (HostGroup& g : gs) {
+          int64_t ch = 0;
+          for (const HostTerm& t : g.terms) ch += stages(t);
+          if (ch <= target + target / 2 || g.terms.size() < 2) {
+            out.push_back(std::move(g));
+            continue;
+          }
+          gofmm::ChainReduce red{};
+          red.dst_row = g.c_row;
+          red.M = g.M;
+          red.src_first = int32_t(H->reduce_src.size());
+          size_t t0 = 0;
+          bool first = true;
+          while (t0 < g.terms.size()) {
+            size_t t1 = t0;
+            int64_t acc = 0;
+            while (t1 < g.terms.size() && (acc < target || t1 == t0)) acc += stages(g.terms[t1++]);
+            HostGroup seg;
+            seg.M = g.M;
+            seg.terms.assign(g.terms.begin() + int64_t(t0), g.terms.begin() + int64_t(t1));
+            if (first) {
+              seg.c_row = g.c_row;
+              first = false;
+            } else {
+              seg.c_row = H->ld_s + H->scratch_rows;  // scratch rows after all nodes
+              H->scratch_rows += pad16(g.M);
+              H->reduce_src.push_back(seg.c_row);
+              ++red.nsrc;
+            }
+            out.push_back(std::move(seg));
+            t0 = t1;
+          }
+          if (red.nsrc > 0) H->reduces.push_back(red);
+        }
+        gs = std::move(out);
+      }
+    }
     push_launch(gs, any_gen, Buf::C, 1, lev);
+    if (!H->launches.empty() && H->launches.back().phase == 1 && H->launches.back().level == lev) {
+      H->launches.back().reduce_first = first_reduce;
+      H->launches.back().reduce_n = int(H->reduces.size()) - first_reduce;
+    }
   }
 
   // output: D, near blocks (ascending index), proj^T c (evaluate.hpp:113-117,196-217)
@@ -1270,6 +1335,12 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_gw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_gw)));
   }
   H->d_tiles.upload(H->tiles);
+  // split-chain scratch rows extend skeleton space (what / c buffers, TMA maps)
+  H->ld_s += pad16(H->scratch_rows);
+  if (!H->reduces.empty()) {
+    H->d_reduces.upload(H->reduces);
+    H->d_reduce_src.upload(H->reduce_src);
+  }
   H->d_groups.alloc(H->groups.size() * sizeof(Group), false);
   size_t nterms = 0;
   for (auto& g : H->groups) nterms += g.terms.size();
@@ -1518,6 +1589,11 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
       if (rows_used) *rows_used = true;
     } else {
       run(L.tfirst[cfg.bm_class], L.tn[cfg.bm_class]);
+    }
+    if (L.reduce_n > 0 && !piece) {  // split term chains: segments 1.. into the group rows
+      dim3 grid(unsigned(L.reduce_n), 8);
+      chain_reduce<<<grid, 256, 0, st>>>(H->d_reduces.as<ChainReduce>() + L.reduce_first,
+                                         H->d_reduce_src.as<int64_t>(), cbase, ldc, r);
     }
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li + 1], st));
   }
@@ -2020,7 +2096,12 @@ int gofmm_launch_profile(const gofmm_handle* H, int32_t r, int32_t cap, gofmm_la
   });
 }
 
-int32_t gofmm_launches_per_eval(const gofmm_handle* H) { return H ? int32_t(H->launches.size()) + 1 : -1; }
+int32_t gofmm_launches_per_eval(const gofmm_handle* H) {
+  if (!H) return -1;
+  int32_t n = int32_t(H->launches.size()) + 1;  // grouped GEMMs + the permutation
+  for (const Launch& L : H->launches) n += L.reduce_n > 0 ? 1 : 0;  // split-chain reductions
+  return n;
+}
 
 int64_t gofmm_device_bytes(const gofmm_handle* H) {
   if (!H) return -1;

@@ -624,6 +624,30 @@ static __global__ void panel_copy(const PanelSeg* __restrict__ segs, double* __r
   }
 }
 
+// Split term chains (latency-bound downward levels): a long group is evaluated as several
+// segment groups, segment 0 into the group's own rows of c and segments 1.. into scratch rows of
+// the same panel buffer; this adds them back, in segment order (deterministic).
+struct ChainReduce {
+  int64_t dst_row;   // 16-aligned row of the group in the panel buffer
+  int32_t M;         // rows
+  int32_t src_first; // first of nsrc scratch rows in the source-row list
+  int32_t nsrc;
+  int32_t pad;
+};
+
+static __global__ void chain_reduce(const ChainReduce* __restrict__ items, const int64_t* __restrict__ src_rows,
+                                    double* __restrict__ c, int64_t pstride, int32_t r) {
+  const ChainReduce it = items[blockIdx.x];
+  const int64_t total = int64_t(it.M) * r;
+  for (int64_t e = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.y) * blockDim.x) {
+    const int m = int(e % it.M), n = int(e / it.M);
+    auto at = [&](int64_t row) -> double& { return c[(row >> 4) * pstride + 16 * int64_t(n) + (row & 15)]; };
+    double acc = at(it.dst_row + m);
+    for (int q = 0; q < it.nsrc; ++q) acc += at(src_rows[it.src_first + q] + m);
+    at(it.dst_row + m) = acc;
+  }
+}
+
 // out[i, c] = sum_p part[p*nrows + i, c]  (fixed order over the partials: deterministic)
 static __global__ void sum_partials(const double* __restrict__ part, int64_t ldp, int32_t nrows, int32_t nparts, int32_t r,
                              double* __restrict__ out, int64_t ldo) {
