@@ -259,7 +259,7 @@ struct Launch {
   std::vector<Part> parts;
 };
 
-constexpr int kOutParts = 4;
+constexpr int kOutParts = 8;
 static_assert(kOutParts <= 8, "per-part D2H timing events (gofmm_handle::dpev)");
 
 // the part boundaries of an output launch: groups split into kOutParts runs of leaves; valid only
