@@ -97,16 +97,17 @@ struct DevBuf {
 // G: generated-operand GEMMs (matrix-free L2L and S2S), r <= 256: 64x256 CTA tile, 16 consumer
 //    warps of 16x64. Every A entry is generated once per CTA and amortised over BN columns.
 // GW: the same for r > 256: 32x512 CTA tile (two 256-column TMA boxes per stage), 16 warps of
-//    16x64, 3 stages. Same accumulator registers and fragment loads per warp as G, but each
-//    generated entry feeds 512 columns instead of 256: entry generation (FP64 ops on the pipe the
-//    DMMAs use) halves per flop. c3: 75.1% -> 81.3% of the FP64 peak.
+//    32x32, 3 stages. Same accumulator registers per warp as G, but each generated entry feeds
+//    512 columns instead of 256: entry generation (FP64 ops on the pipe the DMMAs use) halves per
+//    flop (c3: 75.1% -> 81.3% of the FP64 peak); the 32x32 warp tile needs 8 fragment loads per
+//    16 DMMAs instead of 10 (-> 82.5%; the same change slows G down).
 constexpr int kStagesS = 5, kStagesG = 5, kBM_S = 128, kBN_S = 128, kBM_G = 64, kBN_G = 256;
 constexpr int kStagesGW = 3, kBM_GW = 32, kBN_GW = 512;
 // GN64 / GN128: the same 64-row tiles for r <= 64 / r <= 128 (config 1: r = 64), so no CTA
 // multiplies zero columns and each k-stage is 4x / 2x shorter along the serial term chain.
 #define CFG_S kBM_S, kBN_S, 4, 4, kStagesS
 #define CFG_G kBM_G, kBN_G, 4, 4, kStagesG
-#define CFG_GW kBM_GW, kBN_GW, 2, 8, kStagesGW
+#define CFG_GW kBM_GW, kBN_GW, 1, 16, kStagesGW
 #define CFG_GN64 kBM_G, 64, 4, 4, kStagesG
 #define CFG_GN128 kBM_G, 128, 4, 4, kStagesG
 // GN64W: 32-row tiles for r <= 64 — twice the CTAs and half the stage of GN64 for the
