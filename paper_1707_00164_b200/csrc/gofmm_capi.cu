@@ -1581,7 +1581,9 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
       cfg.fn<<<grid, kThreadsG, cfg.smem, st>>>(*cfg.maps, H->d_tiles.as<Tile>() + t0, H->d_groups.as<Group>(),
                                                  H->d_terms.as<Term>(), r, H->kp, cbase, ldc, cpanel, n_off);
     };
-    if (rows_done && stage == 0 && L.out == Buf::Out && !L.parts.empty()) {
+    // split only launches of many waves: on small trees the extra launches cost more than the
+    // download they hide (config 1: 128 output tiles)
+    if (rows_done && stage == 0 && L.out == Buf::Out && !L.parts.empty() && L.tn[1] >= 8 * H->num_sms) {
       for (size_t p = 0; p + 1 < L.parts.size(); ++p) {
         const Launch::Part &a = L.parts[p], &b = L.parts[p + 1];
         run(a.tile[cfg.bm_class], b.tile[cfg.bm_class] - a.tile[cfg.bm_class]);
@@ -1778,7 +1780,7 @@ void enqueue_chunk32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, 
     const size_t li = size_t(&L - H->launches.data());
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li], st));
     const f32::GemmKernel& k = L.gen ? H->k32_g : H->k32_s;
-    if (rows_done && stage == 0 && L.out == Buf::Out && !L.parts.empty()) {
+    if (rows_done && stage == 0 && L.out == Buf::Out && !L.parts.empty() && L.ntiles32 >= 8 * H->num_sms) {
       for (size_t p = 0; p + 1 < L.parts.size(); ++p) {
         const int t0 = L.parts[p].tile32, nt = L.parts[p + 1].tile32 - t0;
         if (nt > 0)
