@@ -126,6 +126,15 @@ typedef struct gofmm_handle gofmm_handle;
 /* Build the device-resident flattened tree. opts may be NULL (defaults). */
 int gofmm_create(const gofmm_tree_desc* desc, const gofmm_options* opts, gofmm_handle** out);
 
+/* Concurrency (concurrent evaluate() calls on one HMatrix with different w are
+ * allowed): every call on a handle may come from any thread. Calls are serialised on the handle
+ * (host side), and each enqueue waits for the previous one's device work on the handle's
+ * workspace, whatever stream either was issued on — so results are bitwise those of the same
+ * calls made one after another. Device-buffer calls still return before their work completes;
+ * the caller's stream orders its own buffers.
+ * Handles created by gofmm_create_dist with nranks > 1 hold one rank's share of the tree: the
+ * whole-matrix evaluate entry points reject them (GOFMM_ERR_INVALID). */
+
 /* u_perm = K~ w with HOST buffers (pinned or pageable); the drop-in for gfmm::evaluate. */
 int gofmm_evaluate(gofmm_handle* h, const double* w, int64_t ldw, int32_t r, double* u_perm,
                    int64_t ldu, gofmm_eval_stats* stats);
@@ -178,12 +187,14 @@ int gofmm_launch_profile(const gofmm_handle* h, int32_t r, int32_t cap, gofmm_la
  * nranks = 2^l GPUs; the tree is split at level s = l + up to 3 (split_level), and rank g owns a
  * contiguous, work-balanced run of the level-s subtrees (permuted rows [own_row_begin,
  * own_row_end)); nodes above level s are evaluated redundantly on every rank.
+ * W is replicated: every rank receives the full N x r input and permutes all of it, so the W rows
+ * of cross-subtree near-field partners are never exchanged.
  * One all-gather per evaluation: stage1 packs this rank's exports (the skeleton weights `what`
- * other ranks need — all level-s nodes plus cross-subtree far-field partners — and the W rows
- * of leaves that are cross-subtree near-field partners) into a send buffer of
- * max_send_rows x r doubles; the caller all-gathers the nranks send buffers (e.g. ncclAllGather
- * via torch.distributed) into recv (nranks * max_send_rows * r doubles, rank order); stage2
- * consumes it and writes this rank's rows of u_perm. No reduction of outputs is needed. */
+ * other ranks need — all level-s nodes plus cross-subtree far-field partners) into a send buffer
+ * of max_send_rows x r doubles; the nranks send buffers are all-gathered into recv
+ * (nranks * max_send_rows * r doubles, rank order) — by the library (gofmm_dist_evaluate, below)
+ * or by the caller between gofmm_dist_stage1 and gofmm_dist_stage2 — and stage2 consumes it and
+ * writes this rank's rows of u_perm. No reduction of outputs is needed. */
 typedef struct gofmm_dist_info {
   int32_t rank, nranks, split_level, n_exports;
   int64_t send_rows;          /* rows (multiple of 16) this rank exports */
@@ -205,6 +216,27 @@ int gofmm_dist_stage1(gofmm_handle* h, const double* d_w, int64_t ldw, int32_t r
 /* d_recv: nranks x max_send_rows x r doubles (all-gathered); writes u_perm rows of this rank. */
 int gofmm_dist_stage2(gofmm_handle* h, const double* d_recv, int32_t r, double* d_u_perm, int64_t ldu, void* stream);
 
+/* In-library data plane: one call per evaluation on every rank. Stage 1 (permutation of the full
+ * replicated W, own-subtree N2S, pack of the exported skeleton weights) -> ncclAllGather on a
+ * high-priority stream of the handle -> unpack, top-of-tree N2S, downward pass and the proj^T c
+ * output terms; the own leaves' D + near output terms read only W and run on `stream` while the
+ * all-gather is in flight. u_perm receives this rank's rows [own_row_begin, own_row_end).
+ * The communicator is either created by the library from a unique id that rank 0 obtained with
+ * gofmm_nccl_unique_id and the caller broadcast (gofmm_dist_init_comm — collective over all
+ * ranks), or borrowed (gofmm_dist_attach_comm: an ncclComm_t of the NCCL instance loaded in the
+ * process, e.g. torch's ProcessGroupNCCL._comm_ptr(); its size / rank must match the handle).
+ * NCCL is resolved at run time (the already-loaded libnccl.so.2 first); without it these calls
+ * fail with GOFMM_ERR_CUDA. A single-rank handle needs no communicator.
+ * timed != 0 synchronises and fills ms3 = {stage 1, all-gather, whole evaluation} (ms). */
+#define GOFMM_NCCL_UNIQUE_ID_BYTES 128
+int gofmm_nccl_unique_id(void* id_out /* GOFMM_NCCL_UNIQUE_ID_BYTES */);
+int gofmm_dist_init_comm(gofmm_handle* h, const void* unique_id);
+int gofmm_dist_attach_comm(gofmm_handle* h, void* nccl_comm);
+int gofmm_dist_evaluate(gofmm_handle* h, const double* d_w, int64_t ldw, int32_t r, double* d_u_perm, int64_t ldu,
+                        void* stream, int32_t timed, double* ms3);
+int gofmm_dist_evaluate_f32(gofmm_handle* h, const float* d_w, int64_t ldw, int32_t r, float* d_u_perm,
+                            int64_t ldu, void* stream, int32_t timed, double* ms3);
+
 /* FP32 handles: the same two stages; the send buffer is 2 * max_send_rows * r floats (hi then
  * lo halves of the 3xTF32 operands), recv is nranks of those slots in rank order. */
 int gofmm_dist_stage1_f32(gofmm_handle* h, const float* d_w, int64_t ldw, int32_t r, float* d_send, void* stream);
@@ -220,6 +252,11 @@ int gofmm_exact_rows(gofmm_handle* h, const int32_t* rows, int32_t nrows, const 
  * row sample (min(sample_rows, n) rows), then W column-major (host). w_out may be NULL. */
 int gofmm_rng_eps2_draw(uint64_t seed, int32_t n, int32_t r, int32_t sample_rows, int32_t* rows_out, double* w_out,
                         int64_t ldw);
+/* The same draws for resample `attempt` (0, 1, 2): error_eps2 redraws W from the same stream up to
+ * three times while the sampled rows of K W vanish (evaluate.hpp:343-372); attempt a's W follows
+ * the r * n normals of attempts 0..a-1. rows_out may be NULL. */
+int gofmm_rng_eps2_draw_attempt(uint64_t seed, int32_t n, int32_t r, int32_t sample_rows, int32_t attempt,
+                                int32_t* rows_out, double* w_out, int64_t ldw);
 
 /* ---- compress-side skeletonisation ------------------------------------
  * Replaces gfmm::skeletonize_node (compress.hpp:149-187) for a batch of nodes: column-pivoted

@@ -5,15 +5,32 @@
 // (evaluate.hpp:287-317: W in original order, Potentials.u in permuted order, the reference flop
 // counter, std::invalid_argument on bad W) on the B200 through the C-ABI of gofmm_b200.h:
 //
-//   gfmm::B200Evaluator gpu(h);                 // stored blocks, any EntryOracle
-//   gfmm::Potentials p = gpu.evaluate(w);       // == gfmm::evaluate(h, w) to 1e-12 (fp64)
-//   gfmm::Potentials q = gfmm::evaluate_b200(gpu, w, opts);  // evaluate()-shaped free function
+//   gfmm::Potentials p = gfmm::evaluate_b200(h, w, opts);   // evaluate(h, w, opts)'s exact signature
+//   gfmm::ErrorReport e = gfmm::error_eps2_b200(h, oracle, r, rows, seed, opts);  // error_eps2's
 //
-// A Gaussian kernel tree can instead be evaluated matrix-free (near/far blocks regenerated from
-// the coordinates on the device) with B200Evaluator(h, &points, bandwidth).
+// evaluate_b200(h, ...) keeps one device-resident evaluator per HMatrix (stored blocks, any
+// EntryOracle), created on first use and reused by every later call on the same HMatrix — from
+// any thread: SPEC.md:429 concurrent calls are serialised on the device handle (gofmm_b200.h).
+// error_eps2's body (evaluate.hpp:348) is the one place the reference calls evaluate(); routing
+// it to the GPU means calling error_eps2_b200 instead, which draws the same rows and W from the
+// same Rng stream (incl. the up-to-3 redraws) and evaluates them with evaluate_b200.
+//
+// Explicit evaluators: B200Evaluator gpu(h) (stored blocks), or matrix-free — near / far blocks
+// regenerated from the coordinates on the device — for the reference kernel oracles:
+//   B200Evaluator(h, &points, bandwidth)                           Gaussian   oracle.hpp:141-163
+//   B200Evaluator(h, &points, GOFMM_KERNEL_LAPLACE, delta)          Laplace    oracle.hpp:165-195
+//   B200Evaluator(h, &points, GOFMM_KERNEL_POLYNOMIAL, c, degree)   Polynomial oracle.hpp:197-219
+//   B200Evaluator(h, &points, GOFMM_KERNEL_EXPONENTIAL, h)          Matern-1/2 (BASELINE config 4)
+//   B200Evaluator::matrix_free(h, laplace_oracle)                   from the oracle object itself
 #ifndef GOFMM_B200_GFMM_HPP
 #define GOFMM_B200_GFMM_HPP
 
+#include <cmath>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <tuple>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -25,10 +42,20 @@ namespace gfmm {
 class B200Evaluator {
  public:
   /// Stored blocks exactly as HMatrix holds them (leaf_diag, near_field[t].k, far_field[t].k).
-  explicit B200Evaluator(const HMatrix& h, int device = 0) { build(h, nullptr, 0.0, device); }
+  explicit B200Evaluator(const HMatrix& h, int device = 0) { build(h, nullptr, -1, 0.0, 0.0, device); }
   /// Gaussian kernel tree evaluated matrix-free from the point coordinates (oracle.hpp:148-159).
   B200Evaluator(const HMatrix& h, const PointCloud* points, double bandwidth, int device = 0) {
-    build(h, points, bandwidth, device);
+    build(h, points, GOFMM_KERNEL_GAUSSIAN, bandwidth, 0.0, device);
+  }
+  /// Any GOFMM_KERNEL_* evaluated matrix-free (kparam p0, p1 as in gofmm_tree_desc::kparam).
+  B200Evaluator(const HMatrix& h, const PointCloud* points, int kernel, double p0, double p1 = 0.0,
+                int device = 0) {
+    if (!points) throw std::invalid_argument("matrix-free evaluation needs the point cloud");
+    build(h, points, kernel, p0, p1, device);
+  }
+  /// Matrix-free from the reference oracle object (its points and parameter).
+  static std::unique_ptr<B200Evaluator> matrix_free(const HMatrix& h, const LaplaceKernelOracle& k, int device = 0) {
+    return std::make_unique<B200Evaluator>(h, &k.points(), GOFMM_KERNEL_LAPLACE, k.regularization(), 0.0, device);
   }
   B200Evaluator(const B200Evaluator&) = delete;
   B200Evaluator& operator=(const B200Evaluator&) = delete;
@@ -55,7 +82,7 @@ class B200Evaluator {
   }
 
  private:
-  void build(const HMatrix& h, const PointCloud* pts, double bandwidth, int device) {
+  void build(const HMatrix& h, const PointCloud* pts, int kernel, double p0, double p1, int device) {
     const MetricTree& t = h.tree;
     n_ = h.n;
     const int nn = static_cast<int>(t.nodes.size());
@@ -122,11 +149,13 @@ class B200Evaluator {
     d.far_a = fa_.data();
     d.far_b = fb_.data();
     if (pts) {
+      if (pts->size() != h.n) throw std::invalid_argument("point cloud size differs from the HMatrix");
       d.source = GOFMM_SOURCE_KERNEL;
-      d.kernel = GOFMM_KERNEL_GAUSSIAN;
+      d.kernel = kernel;
       d.dim = pts->dim();
       d.coords = pts->coords.data();
-      d.kparam[0] = bandwidth;
+      d.kparam[0] = p0;
+      d.kparam[1] = p1;
     } else {
       d.source = GOFMM_SOURCE_STORED;
       d.diag_offset = diag_off_.data();
@@ -154,6 +183,114 @@ class B200Evaluator {
 /// change results in the reference (evaluate.hpp:118) and are not needed here.
 inline Potentials evaluate_b200(const B200Evaluator& gpu, const Matrix& w, const EvalOptions& = {}) {
   return gpu.evaluate(w);
+}
+
+namespace b200_detail {
+// One device-resident evaluator per HMatrix. The key is the HMatrix's address plus a fingerprint
+// of what it owns (sizes and the addresses of its block storage), so a different HMatrix that
+// reuses a freed address is rebuilt rather than served a stale tree.
+struct CacheKey {
+  const HMatrix* h;
+  int n;
+  size_t nodes, near, far;
+  const double* diag0;
+  const double* proj0;
+  bool operator<(const CacheKey& o) const {
+    return std::tie(h, n, nodes, near, far, diag0, proj0) < std::tie(o.h, o.n, o.nodes, o.near, o.far, o.diag0, o.proj0);
+  }
+};
+inline CacheKey key_of(const HMatrix& h) {
+  const double* d0 = nullptr;
+  for (const Matrix& m : h.leaf_diag)
+    if (m.size()) {
+      d0 = m.data();
+      break;
+    }
+  const double* p0 = nullptr;
+  for (const Skeleton& sk : h.skeletons)
+    if (sk.valid() && sk.proj.size()) {
+      p0 = sk.proj.data();
+      break;
+    }
+  return {&h, h.n, h.tree.nodes.size(), h.near_field.size(), h.far_field.size(), d0, p0};
+}
+inline std::mutex& cache_mutex() {
+  static std::mutex m;
+  return m;
+}
+inline std::map<CacheKey, std::shared_ptr<B200Evaluator>>& cache() {
+  static std::map<CacheKey, std::shared_ptr<B200Evaluator>> c;
+  return c;
+}
+inline std::shared_ptr<B200Evaluator> evaluator_for(const HMatrix& h) {
+  const CacheKey k = key_of(h);
+  std::lock_guard<std::mutex> g(cache_mutex());
+  auto& c = cache();
+  auto it = c.find(k);
+  if (it != c.end()) return it->second;
+  for (auto i = c.begin(); i != c.end();)  // same address, different contents: stale
+    i = (i->first.h == &h) ? c.erase(i) : std::next(i);
+  auto ev = std::make_shared<B200Evaluator>(h);
+  c.emplace(k, ev);
+  return ev;
+}
+}  // namespace b200_detail
+
+/// Drop the cached device copy of `h` (call before destroying an HMatrix to free HBM early).
+inline void b200_release(const HMatrix& h) {
+  std::lock_guard<std::mutex> g(b200_detail::cache_mutex());
+  auto& c = b200_detail::cache();
+  for (auto i = c.begin(); i != c.end();) i = (i->first.h == &h) ? c.erase(i) : std::next(i);
+}
+
+/// evaluate(h, w, opts) (evaluate.hpp:287-317) on the B200, same signature and contract.
+inline Potentials evaluate_b200(const HMatrix& h, const Matrix& w, const EvalOptions& opts = {}) {
+  if (w.rows() != h.n) throw std::invalid_argument("evaluate: w has wrong row count");
+  if (w.cols() < 1) throw std::invalid_argument("evaluate: w needs at least one column");
+  return evaluate_b200(*b200_detail::evaluator_for(h), w, opts);
+}
+
+/// error_eps2(h, oracle, r, sample_rows, seed, opts) (evaluate.hpp:330-373) with its evaluate()
+/// routed to the B200: the same sampled rows and W (the reference Rng stream, restated in the
+/// C-ABI: gofmm_rng_eps2_draw_attempt), up to three draws while the sampled rows of K w vanish,
+/// exact rows from the caller's oracle on the host, the same report fields.
+inline ErrorReport error_eps2_b200(const HMatrix& h, const EntryOracle& oracle, int r, int sample_rows,
+                                   std::uint64_t seed, const EvalOptions& opts = {}) {
+  if (sample_rows < 1) throw std::invalid_argument("sample_rows must be >= 1");
+  if (r < 1) throw std::invalid_argument("r must be >= 1");
+  const int n = h.n;
+  const int k = std::min(sample_rows, n);
+  ErrorReport rep;
+  rep.sample_rows.resize(k);
+  IndexList all(n);
+  std::iota(all.begin(), all.end(), 0);
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    Matrix w(n, r);
+    if (gofmm_rng_eps2_draw_attempt(seed, n, r, sample_rows, attempt, rep.sample_rows.data(), w.data(), n) !=
+        GOFMM_OK)
+      throw std::runtime_error(std::string("gofmm_rng_eps2_draw_attempt: ") + gofmm_last_error());
+    const Potentials pot = evaluate_b200(h, w, opts);
+    const Matrix u = unpermute(h.tree, pot.u);
+    rep.eval_flops = pot.flops;
+    rep.eval_seconds = pot.seconds;
+    const Matrix exact = oracle.block(rep.sample_rows, all) * w;
+    double num = 0.0, den = 0.0;
+    std::vector<double> rel;
+    rel.reserve(k);
+    for (int t = 0; t < k; ++t) {
+      const double dn = (u.row(rep.sample_rows[t]) - exact.row(t)).norm();
+      const double de = exact.row(t).norm();
+      num += dn * dn;
+      den += de * de;
+      rel.push_back(de > 0 ? dn / de : 0.0);
+    }
+    if (den == 0.0) continue;
+    rep.eps2 = std::sqrt(num / den);
+    rep.per_entry.assign(rel.begin(), rel.begin() + std::min<size_t>(10, rel.size()));
+    rep.mean_sample = std::accumulate(rel.begin(), rel.end(), 0.0) / double(rel.size());
+    return rep;
+  }
+  throw numeric_error("error_eps2: sampled rows of Kw vanished repeatedly");
 }
 
 }  // namespace gfmm

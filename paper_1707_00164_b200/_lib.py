@@ -61,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for cmd, p in procs:
         if p.wait() != 0:
             raise subprocess.CalledProcessError(p.returncode, cmd)
-    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB_PATH, *objs]
+    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB_PATH, *objs, "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
@@ -134,7 +134,8 @@ EXPORTS = ("gofmm_create", "gofmm_evaluate", "gofmm_evaluate_device", "gofmm_unp
            "gofmm_rng_eps2_draw", "gofmm_evaluate_f32", "gofmm_evaluate_device_f32",
            "gofmm_unpermute_device_f32", "gofmm_precision", "gofmm_dist_stage1_f32", "gofmm_dist_stage2_f32",
            "gofmm_skeletonize_batch", "gofmm_skeletonize_last_error", "gofmm_ann_leaf_merge",
-           "gofmm_ann_last_error")
+           "gofmm_ann_last_error", "gofmm_rng_eps2_draw_attempt", "gofmm_nccl_unique_id", "gofmm_dist_init_comm",
+           "gofmm_dist_attach_comm", "gofmm_dist_evaluate", "gofmm_dist_evaluate_f32")
 
 
 class SkelStats(C.Structure):
@@ -171,6 +172,13 @@ def lib():
         L.gofmm_dist_stage2_f32.argtypes = [P, P, C.c_int32, P, C.c_int64, P]
         L.gofmm_exact_rows.argtypes = [P, P, C.c_int32, P, C.c_int64, C.c_int32, P, C.c_int64, P]
         L.gofmm_rng_eps2_draw.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, P, P, C.c_int64]
+        L.gofmm_rng_eps2_draw_attempt.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P, P,
+                                                  C.c_int64]
+        L.gofmm_nccl_unique_id.argtypes = [P]
+        L.gofmm_dist_init_comm.argtypes = [P, P]
+        L.gofmm_dist_attach_comm.argtypes = [P, P]
+        L.gofmm_dist_evaluate.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, P, C.c_int32, P]
+        L.gofmm_dist_evaluate_f32.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, P, C.c_int32, P]
         L.gofmm_device_bytes.argtypes = [P]
         L.gofmm_device_bytes.restype = C.c_int64
         L.gofmm_launches_per_eval.argtypes = [P]

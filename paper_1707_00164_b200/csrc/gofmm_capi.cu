@@ -32,6 +32,7 @@
 #include <cstring>
 #include <functional>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -39,6 +40,7 @@
 #include "../../include/gofmm_b200.h"
 #include "gofmm_kernels.cuh"
 #include "gofmm_kernels_f32.cuh"
+#include "nccl_dyn.h"
 
 namespace gofmm {
 namespace {
@@ -214,6 +216,10 @@ void generate_dispatch(int kind, int dim, const double* xr, int rows, const doub
 }
 
 // ---------------------------------------------------------------- plan
+// SM count the split of long downward term chains is sized for (B200: 148). A constant, so the
+// summation order of the result does not depend on the device (see build()).
+constexpr int kSplitRefSms = 148;
+
 enum class Buf { Wp, What, C, Out };  // B operand / output bases (resolved per workspace)
 
 struct HostTerm {
@@ -233,6 +239,7 @@ struct HostGroup {
   int64_t c_row;
   int M;
   std::vector<HostTerm> terms;
+  int flags = 0;  // kGroupLoadC: continue the chain a previous launch left in C
 };
 
 struct Launch {
@@ -246,7 +253,9 @@ struct Launch {
   int phase;  // 0 upward, 1 downward, 2 output
   int level;  // tree level (output launch: -1)
   int64_t flops_per_rhs = 0;  // reference-counted flops of this launch per RHS column
-  int stage = 2;  // distributed evaluation: 1 = before the all-gather (own-subtree N2S), 2 = after
+  // distributed evaluation: 1 = before the all-gather (own-subtree N2S), 2 = after it, 3 = the
+  // own leaves' D + near output terms, which need no exchanged data and run during the all-gather
+  int stage = 2;
   int first_group = 0, ngroups = 0;      // groups [first_group, first_group + ngroups)
   int reduce_first = 0, reduce_n = 0;    // split-chain reductions after this launch (chain_reduce)
   int first_tile32 = 0, ntiles32 = 0;    // FP32 plan: 128-row tiles of the same groups
@@ -428,7 +437,10 @@ DistPlan make_dist_plan(int nranks, int nn, const int32_t* left, const int32_t* 
       // would mean an inconsistent tree
       throw Error(GOFMM_ERR_INVALID, "node below the split without an owning subtree");
     }
-  std::vector<char> need_what(nn, 0), need_w(nn, 0);
+  // W is replicated (every rank receives the full N x r input), so the W rows of cross-subtree
+  // near-field partners are permuted locally in stage 1 and never exchanged; only skeleton weights
+  // (what) travel.
+  std::vector<char> need_what(nn, 0);
   if (nranks > 1) {
     for (int i : at_split) need_what[i] = 1;  // every rank's top N2S needs all level-l what
     auto request = [&](int requester_node, int target) {
@@ -440,28 +452,15 @@ DistPlan make_dist_plan(int nranks, int nn, const int32_t* left, const int32_t* 
       request(far_a[t], far_b[t]);
       request(far_b[t], far_a[t]);
     }
-    for (int64_t t = 0; t < n_near; ++t) {
-      const int a = near_a[t], b = near_b[t];
-      if (P.owner[a] != P.owner[b]) need_w[a] = need_w[b] = 1;
-    }
   }
-  // skeleton / point space offsets (same formulas as build())
-  std::vector<int64_t> soff(nn, -1), pst(nn, -1);
+  // skeleton space offsets (same formula as build())
+  std::vector<int64_t> soff(nn, -1);
   int64_t off = 0;
   for (int i = 0; i < nn; ++i)
     if (rank[i] >= 0) {
       soff[i] = off;
       off += pad16_(rank[i]);
     }
-  std::vector<int32_t> leaves;
-  for (int i = 0; i < nn; ++i)
-    if (left[i] < 0) leaves.push_back(i);
-  std::sort(leaves.begin(), leaves.end(), [&](int a, int b) { return start[a] < start[b]; });
-  off = 0;
-  for (int i : leaves) {
-    pst[i] = off;
-    off += pad16_(end[i] - start[i]);
-  }
   P.exports.assign(nranks, {});
   P.send_rows.assign(nranks, 0);
   for (int i = 0; i < nn; ++i)
@@ -469,8 +468,6 @@ DistPlan make_dist_plan(int nranks, int nn, const int32_t* left, const int32_t* 
       if (rank[i] < 0) throw Error(GOFMM_ERR_INVALID, "exported node has no skeleton");
       P.exports[P.owner[i]].push_back({0, soff[i], pad16_(rank[i])});
     }
-  for (int i : leaves)
-    if (need_w[i]) P.exports[P.owner[i]].push_back({1, pst[i], pad16_(end[i] - start[i])});
   for (int g = 0; g < nranks; ++g) {
     for (const Seg& sg : P.exports[g]) P.send_rows[g] += sg.rows;
     P.max_send_rows = std::max(P.max_send_rows, P.send_rows[g]);
@@ -482,6 +479,12 @@ DistPlan make_dist_plan(int nranks, int nn, const int32_t* left, const int32_t* 
 }  // namespace gofmm
 
 struct gofmm_handle {
+  // SPEC.md:429 allows concurrent evaluate() calls on one HMatrix. Every entry point that touches
+  // the plan, workspace or timing state holds `mu` (host side), and every enqueue waits on
+  // `ws_free` before its first launch and records it after its last, so evaluations issued on
+  // different streams (or threads) never overlap on the shared device workspace.
+  mutable std::mutex mu;
+  cudaEvent_t ws_free = nullptr;
   int device = 0;
   int num_sms = 148;  // launch-config costing (queried at create)
   cudaStream_t stream = nullptr;
@@ -543,6 +546,14 @@ struct gofmm_handle {
   int64_t own_begin = 0, own_end = 0;          // own permuted rows [start, end)
   int64_t full_flops_per_rhs = 0;              // the whole (undistributed) evaluation
   gofmm::DevBuf d_segs;                        // pack / unpack segment table
+  // in-library data plane (gofmm_dist_evaluate): the NCCL communicator over the nranks GPUs
+  // (owned when created from a unique id), a high-priority stream for the all-gather, the send /
+  // receive slots, and the events that order stage 1 -> all-gather -> stage 4
+  gofmm::nccl::comm_t comm = nullptr;
+  bool own_comm = false;
+  cudaStream_t s_comm = nullptr;
+  cudaEvent_t ev_pack = nullptr, ev_gath = nullptr, dtev[4] = {};
+  gofmm::DevBuf d_send, d_recv;
   std::vector<double> coords_host;             // d x n original order (kernel sources; exact rows)
   gofmm::DevBuf d_ex_groups, d_ex_terms, d_ex_tiles, d_ex_x, d_ex_part;  // exact-rows scratch
   int32_t n_pack = 0, n_unpack = 0;
@@ -721,6 +732,7 @@ void build_f32(gofmm_handle* H) {
     Group g{};
     g.crow = hg.c_row;
     g.M = hg.M;
+    g.flags = hg.flags;
     g.tbeg = int(ts.size());
     for (const HostTerm& ht : hg.terms) {
       f32::Term t{};
@@ -1170,17 +1182,24 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     // per-SM share into segments of about that share. Segment 0 accumulates into the group's own
     // rows, the others into scratch rows appended to skeleton space; chain_reduce adds them in
     // segment order after the launch. FP64 only (the FP32 epilogue stores hi/lo operands).
+    // The split (and so the summation order of c) is a function of the WHOLE level and a fixed SM
+    // count only — never of this device's SM count or of a rank's share of the level — so u is
+    // bitwise the same on any GPU SKU and for every rank layout of the subtree split.
     const int first_reduce = int(H->reduces.size());
     if (H->precision == GOFMM_PRECISION_F64 && !gs.empty()) {
       auto stages = [](const HostTerm& t) { return int64_t((t.K + 15) / 16); };
+      auto kstages = [](int64_t k) { return (k + 15) / 16; };
       int64_t sum = 0, mx = 0;
-      for (const HostGroup& g : gs) {
+      for (int i = 0; i < nn; ++i) {  // every node of the level, owned or not
+        if (H->level[i] != lev || H->rank[i] < 0) continue;
         int64_t ch = 0;
-        for (const HostTerm& t : g.terms) ch += stages(t);
-        sum += ch * ((std::max(g.M, 0) + kBM_G - 1) / kBM_G);
+        for (const Partner& p : partners[i]) ch += kstages(H->rank[p.other]);
+        const int par = H->parent[i];
+        if (par > 0 && H->rank[par] >= 0) ch += kstages(H->rank[par]);
+        sum += ch * ((H->rank[i] + kBM_G - 1) / kBM_G);
         mx = std::max(mx, ch);
       }
-      const double fair = double(sum) / double(H->num_sms);
+      const double fair = double(sum) / double(kSplitRefSms);
       if (double(mx) > 2.0 * fair && mx >= 24) {
         const int64_t target = std::max<int64_t>(8, int64_t(std::ceil(fair)));
         std::vector<HostGroup> out;
@@ -1230,7 +1249,12 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
 
   // output: D, near blocks (ascending index), proj^T c (evaluate.hpp:113-117,196-217)
   {
-    std::vector<HostGroup> gs;
+    // A rank of an FP64 subtree split runs the chain in two launches: D + near terms (stage 3,
+    // inputs all local: W is replicated) while the all-gather is in flight, then proj^T c
+    // (stage 2) continuing the same accumulators from u (kGroupLoadC) — bitwise the one-launch sum.
+    const bool split_out = H->nranks > 1 && H->precision == GOFMM_PRECISION_F64;
+    std::vector<HostGroup> gs, gs_proj;
+    int64_t flops_proj = 0;
     for (int id : H->leaf_ids) {
       if (H->dist.owner[id] != H->drank) continue;
       HostGroup g;
@@ -1286,12 +1310,27 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
         v.b_buf = Buf::C;
         v.b_row = H->soff[id];
         v.K = H->rank[id];
-        flops += 2LL * H->rank[id] * n_a;
-        g.terms.push_back(v);
+        if (split_out) {
+          HostGroup gp;
+          gp.c_row = g.c_row;
+          gp.M = g.M;
+          gp.flags = kGroupLoadC;
+          gp.terms.push_back(v);
+          gs_proj.push_back(std::move(gp));
+          flops_proj += 2LL * H->rank[id] * n_a;
+        } else {
+          flops += 2LL * H->rank[id] * n_a;
+          g.terms.push_back(v);
+        }
       }
       gs.push_back(std::move(g));
     }
     push_launch(gs, gen_near, Buf::Out, 2, -1);
+    if (split_out) {
+      if (!H->launches.empty() && H->launches.back().out == Buf::Out) H->launches.back().stage = 3;
+      flops += flops_proj;
+      push_launch(gs_proj, false, Buf::Out, 2, -1);
+    }
   }
   H->flops_per_rhs = flops;
   {
@@ -1400,6 +1439,7 @@ void upload_plan(gofmm_handle* H) {
     Group g{};
     g.crow = hg.c_row;
     g.M = hg.M;
+    g.flags = hg.flags;
     g.tbeg = int(ts.size());
     for (const HostTerm& ht : hg.terms) {
       Term t{};
@@ -1513,6 +1553,19 @@ LaunchCfg pick_launch_cfg(const gofmm_handle* H, const Launch& L, int32_t r) {
   return c[best].cfg;
 }
 
+// Which plan launches an enqueue of `stage` runs. 0: a whole single-GPU evaluation; the two-call
+// distributed API: 1 (before the all-gather) and 2 (after it: stage-2 and stage-3 launches);
+// gofmm_dist_evaluate splits the second half into 3 (own D + near output terms, overlapping the
+// all-gather) and 4 (the rest, after it).
+inline bool stage_runs(int stage, int launch_stage) {
+  switch (stage) {
+    case 0: return true;
+    case 2: return launch_stage == 2 || launch_stage == 3;
+    case 4: return launch_stage == 2;
+    default: return launch_stage == stage;
+  }
+}
+
 // rows_done (host-buffer pipeline, stage 0 only): called after each part of a split output
 // launch is enqueued, with the u_perm rows that part completes; returns whether it was used.
 using RowsDone = std::function<void(int64_t row0, int64_t row1)>;
@@ -1529,18 +1582,20 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
   upload_plan(H);
   encode_maps(H, r);
   if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[0], st));
-  if (stage == 2 && H->n_unpack > 0) {
+  if ((stage == 2 || stage == 4) && H->n_unpack > 0) {
     // ghosts: every other rank's exported what / W rows into their places in this workspace
     dim3 grid(unsigned(H->n_unpack), 8);
     panel_copy<<<grid, 256, 0, st>>>(H->d_segs.as<PanelSeg>() + H->n_pack, H->d_what.as<double>(),
                                      H->d_wp.as<double>(), int64_t(H->ws_r) * 16, d_xbuf, r, 0);
   }
-  if (stage != 2 && phase_lo == 0) {
+  if ((stage == 0 || stage == 1) && phase_lo == 0) {
     // K5: row gather into the padded leaf layout (evaluate.hpp:294-295). Blocks walk all rows of
     // cpb columns before the next columns (grid.x = rows), so the randomly gathered source
     // columns (N * cpb * 8 bytes) stay L2-resident: each 32-byte sector is fetched from HBM once.
+    // Stage 1 permutes every row too: W is replicated, so the near-field partners' rows a rank
+    // needs come from its own copy of W instead of the all-gather.
     const int cpb = int(std::max<int64_t>(1, std::min<int64_t>(8, (48ll << 20) / (int64_t(H->n) * 8))));
-    const int64_t row0 = stage == 1 ? H->own_pst_begin : 0, row1 = stage == 1 ? H->own_pst_end : H->ld_wp;
+    const int64_t row0 = 0, row1 = H->ld_wp;
     const int32_t pc0 = piece ? c0 : 0, pr = piece ? c1 - c0 : r;  // columns of this piece
     if (row1 > row0 && pr > 0) {
       dim3 grid(unsigned((row1 - row0 + 255) / 256), unsigned((pr + cpb - 1) / cpb));
@@ -1552,7 +1607,7 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
   if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[1], st));
   int marked = 1;
   for (const Launch& L : H->launches) {
-    if (stage != 0 && L.stage != stage) continue;
+    if (!stage_runs(stage, L.stage)) continue;
     if (piece && L.phase != 0) continue;
     if (L.phase < phase_lo) {  // ran in the column pieces: zero-length timing pair
       const size_t li = size_t(&L - H->launches.data());
@@ -1755,19 +1810,19 @@ void enqueue_chunk32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, 
   prepare32(H, r);
   const int64_t pstride = int64_t(H->ws32_r) * 16;
   if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[0], st));
-  if (stage == 2 && H->n_unpack > 0)  // ghosts: other ranks' exported what / W rows
+  if ((stage == 2 || stage == 4) && H->n_unpack > 0)  // ghosts: other ranks' exported what
     GOFMM_CUDA(f32::launch_panel_copy(H->d_segs.as<PanelSeg>() + H->n_pack, H->n_unpack, H->d_what32[0].as<float>(),
                                       H->d_what32[1].as<float>(), H->d_wp32[0].as<float>(), H->d_wp32[1].as<float>(),
                                       pstride, d_xbuf, r, H->dist.max_send_rows, 0, st));
-  if (stage != 2) {
-    const int64_t row0 = stage == 1 ? H->own_pst_begin : 0, row1 = stage == 1 ? H->own_pst_end : H->ld_wp;
+  if (stage == 0 || stage == 1) {  // every row, also in stage 1 (W is replicated, see enqueue_chunk)
+    const int64_t row0 = 0, row1 = H->ld_wp;
     GOFMM_CUDA(f32::launch_permute_in(d_w, ldw, H->d_prow.as<int32_t>(), row0, row1, r, H->n,
                                       H->d_wp32[0].as<float>(), H->d_wp32[1].as<float>(), pstride, st));
   }
   if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[1], st));
   int marked = 1;
   for (const Launch& L : H->launches) {
-    if (stage != 0 && L.stage != stage) continue;
+    if (!stage_runs(stage, L.stage)) continue;
     while (timed && marked <= L.phase) GOFMM_CUDA(cudaEventRecord(H->ev[1 + marked++], st));
     float *ch, *cl;
     int64_t ldc;
@@ -1868,6 +1923,26 @@ void check_args(gofmm_handle* H, const void* w, int64_t ldw, int32_t r, const vo
   if (!w || !u) throw Error(GOFMM_ERR_INVALID, "evaluate: null buffer");
 }
 
+// A subtree-split handle holds only its rank's groups: a whole-matrix evaluation on it would
+// leave other ranks' rows of u unwritten and read what rows nobody computed.
+void check_single(const gofmm_handle* H) {
+  if (H->nranks > 1)
+    throw Error(GOFMM_ERR_INVALID,
+                "evaluate: handle is one rank of a subtree split (nranks > 1); use gofmm_dist_evaluate "
+                "or gofmm_dist_stage1 / gofmm_dist_stage2");
+}
+
+// Ownership of the handle's device workspace for one enqueue on `st` (gofmm_handle::ws_free):
+// wait for the previous enqueue (any stream) to finish with it, release it after ours.
+struct WsGuard {
+  gofmm_handle* H;
+  cudaStream_t st;
+  WsGuard(gofmm_handle* h, cudaStream_t s) : H(h), st(s) { GOFMM_CUDA(cudaStreamWaitEvent(st, H->ws_free, 0)); }
+  ~WsGuard() { cudaEventRecord(H->ws_free, st); }
+  WsGuard(const WsGuard&) = delete;
+  WsGuard& operator=(const WsGuard&) = delete;
+};
+
 }  // namespace
 }  // namespace gofmm
 
@@ -1893,6 +1968,7 @@ int gofmm_create(const gofmm_tree_desc* desc, const gofmm_options* opts, gofmm_h
     GOFMM_CUDA(cudaDeviceGetAttribute(&H->num_sms, cudaDevAttrMultiProcessorCount, H->device));
     GOFMM_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
     for (auto& e : H->ev) GOFMM_CUDA(cudaEventCreate(&e));
+    GOFMM_CUDA(cudaEventCreateWithFlags(&H->ws_free, cudaEventDisableTiming));
     build(H.get(), desc, opts);
     H->lev.assign(2 * H->launches.size(), nullptr);
     for (auto& e : H->lev) GOFMM_CUDA(cudaEventCreate(&e));
@@ -1918,6 +1994,7 @@ int gofmm_create_dist(const gofmm_tree_desc* desc, const gofmm_options* opts, in
     GOFMM_CUDA(cudaDeviceGetAttribute(&H->num_sms, cudaDevAttrMultiProcessorCount, H->device));
     GOFMM_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
     for (auto& e : H->ev) GOFMM_CUDA(cudaEventCreate(&e));
+    GOFMM_CUDA(cudaEventCreateWithFlags(&H->ws_free, cudaEventDisableTiming));
     build(H.get(), desc, opts);
     H->lev.assign(2 * H->launches.size(), nullptr);
     for (auto& e : H->lev) GOFMM_CUDA(cudaEventCreate(&e));
@@ -1995,10 +2072,12 @@ int gofmm_dist_plan_host(const gofmm_tree_desc* d, int32_t rank, int32_t nranks,
 int gofmm_dist_stage1(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double* d_send, void* stream) {
   return guarded([&] {
     check_args(H, d_w, ldw, r, d_w, H->n);
+    std::lock_guard<std::mutex> lk(H->mu);
     check_precision(H, GOFMM_PRECISION_F64);
     if (H->nranks > 1 && !d_send && H->dist.max_send_rows > 0) throw Error(GOFMM_ERR_INVALID, "null send buffer");
     GOFMM_CUDA(cudaSetDevice(H->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    WsGuard ws(H, st);
     enqueue_chunk(H, d_w, ldw, r, nullptr, H->n, st, false, 1, d_send);
   });
 }
@@ -2006,11 +2085,13 @@ int gofmm_dist_stage1(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r
 int gofmm_dist_stage2(gofmm_handle* H, const double* d_recv, int32_t r, double* d_u, int64_t ldu, void* stream) {
   return guarded([&] {
     check_args(H, d_u, H->n, r, d_u, ldu);
+    std::lock_guard<std::mutex> lk(H->mu);
     check_precision(H, GOFMM_PRECISION_F64);
     if (H->nranks > 1 && !d_recv && H->dist.max_send_rows > 0) throw Error(GOFMM_ERR_INVALID, "null receive buffer");
     if (r > H->ws_r) throw Error(GOFMM_ERR_INVALID, "stage2: r differs from stage1");
     GOFMM_CUDA(cudaSetDevice(H->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    WsGuard ws(H, st);
     enqueue_chunk(H, nullptr, H->n, r, d_u, ldu, st, false, 2, const_cast<double*>(d_recv));
   });
 }
@@ -2018,10 +2099,12 @@ int gofmm_dist_stage2(gofmm_handle* H, const double* d_recv, int32_t r, double* 
 int gofmm_dist_stage1_f32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, float* d_send, void* stream) {
   return guarded([&] {
     check_args(H, d_w, ldw, r, d_w, H->n);
+    std::lock_guard<std::mutex> lk(H->mu);
     check_precision(H, GOFMM_PRECISION_F32);
     if (H->nranks > 1 && !d_send && H->dist.max_send_rows > 0) throw Error(GOFMM_ERR_INVALID, "null send buffer");
     GOFMM_CUDA(cudaSetDevice(H->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    WsGuard ws(H, st);
     enqueue_chunk32(H, d_w, ldw, r, nullptr, H->n, st, false, 1, d_send);
   });
 }
@@ -2029,13 +2112,167 @@ int gofmm_dist_stage1_f32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_
 int gofmm_dist_stage2_f32(gofmm_handle* H, const float* d_recv, int32_t r, float* d_u, int64_t ldu, void* stream) {
   return guarded([&] {
     check_args(H, d_u, H->n, r, d_u, ldu);
+    std::lock_guard<std::mutex> lk(H->mu);
     check_precision(H, GOFMM_PRECISION_F32);
     if (H->nranks > 1 && !d_recv && H->dist.max_send_rows > 0) throw Error(GOFMM_ERR_INVALID, "null receive buffer");
     if (r > H->ws32_r) throw Error(GOFMM_ERR_INVALID, "stage2: r differs from stage1");
     GOFMM_CUDA(cudaSetDevice(H->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    WsGuard ws(H, st);
     enqueue_chunk32(H, nullptr, H->n, r, d_u, ldu, st, false, 2, const_cast<float*>(d_recv));
   });
+}
+
+}  // extern "C"
+
+namespace {
+// One distributed evaluation on the handle's own data plane (north_star (4)): stage 1 (full
+// permutation, own-subtree N2S, pack of the exported skeleton weights) -> ncclAllGather on a
+// high-priority stream -> stage 4 (unpack, top-of-tree N2S, downward, proj^T c output). The own
+// leaves' D + near output terms (stage 3) read only W, so they run on `st` WHILE the all-gather
+// is in flight. ms3 (timed): {stage 1, all-gather, whole evaluation} in ms.
+template <class T>
+void dist_evaluate(gofmm_handle* H, const T* d_w, int64_t ldw, int32_t r, T* d_u, int64_t ldu, cudaStream_t st,
+                   bool timed, double* ms3) {
+  constexpr bool kF32 = sizeof(T) == 4;
+  std::string why;
+  const nccl::Api* api = nullptr;
+  if (H->comm) {
+    api = nccl::api(&why);
+    if (!api) throw Error(GOFMM_ERR_CUDA, why);
+  } else if (H->nranks > 1) {
+    throw Error(GOFMM_ERR_INVALID, "gofmm_dist_evaluate: no communicator (gofmm_dist_init_comm / _attach_comm)");
+  }
+  const size_t slot = size_t(H->dist.max_send_rows) * size_t(r) * (kF32 ? 2 : 1);  // elements per rank
+  if (H->d_send.bytes < std::max<size_t>(slot, 1) * sizeof(T)) H->d_send.alloc(std::max<size_t>(slot, 1) * sizeof(T), false);
+  const size_t rbytes = std::max<size_t>(slot * size_t(H->nranks), 1) * sizeof(T);
+  if (H->d_recv.bytes < rbytes) H->d_recv.alloc(rbytes, false);
+  if (!H->ev_pack) {
+    int least = 0, greatest = 0;
+    GOFMM_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    GOFMM_CUDA(cudaStreamCreateWithPriority(&H->s_comm, cudaStreamNonBlocking, greatest));
+    GOFMM_CUDA(cudaEventCreateWithFlags(&H->ev_pack, cudaEventDisableTiming));
+    GOFMM_CUDA(cudaEventCreateWithFlags(&H->ev_gath, cudaEventDisableTiming));
+    for (auto& e : H->dtev) GOFMM_CUDA(cudaEventCreate(&e));
+  }
+  T* send = H->d_send.as<T>();
+  T* recv = H->d_recv.as<T>();
+  if (timed) GOFMM_CUDA(cudaEventRecord(H->dtev[0], st));
+  if constexpr (kF32)
+    enqueue_chunk32(H, d_w, ldw, r, nullptr, H->n, st, false, 1, send);
+  else
+    enqueue_chunk(H, d_w, ldw, r, nullptr, H->n, st, false, 1, send);
+  if (timed) GOFMM_CUDA(cudaEventRecord(H->dtev[1], st));
+  GOFMM_CUDA(cudaEventRecord(H->ev_pack, st));
+  GOFMM_CUDA(cudaStreamWaitEvent(H->s_comm, H->ev_pack, 0));
+  if (timed) GOFMM_CUDA(cudaEventRecord(H->dtev[2], H->s_comm));
+  if (api && slot > 0) {
+    const nccl::result_t rc = api->AllGather(send, recv, slot, kF32 ? nccl::kFloat32 : nccl::kFloat64, H->comm,
+                                             H->s_comm);
+    if (rc != nccl::kSuccess) throw Error(GOFMM_ERR_CUDA, std::string("ncclAllGather: ") + api->GetErrorString(rc));
+  }
+  if (timed) GOFMM_CUDA(cudaEventRecord(H->dtev[3], H->s_comm));
+  GOFMM_CUDA(cudaEventRecord(H->ev_gath, H->s_comm));
+  // own D + near output terms: no exchanged input, overlap the all-gather
+  if constexpr (!kF32) enqueue_chunk(H, nullptr, H->n, r, d_u, ldu, st, false, 3, nullptr);
+  GOFMM_CUDA(cudaStreamWaitEvent(st, H->ev_gath, 0));
+  if constexpr (kF32)
+    enqueue_chunk32(H, nullptr, H->n, r, d_u, ldu, st, false, 4, recv);
+  else
+    enqueue_chunk(H, nullptr, H->n, r, d_u, ldu, st, false, 4, recv);
+  if (timed) {
+    GOFMM_CUDA(cudaEventRecord(H->ev[7], st));
+    GOFMM_CUDA(cudaEventSynchronize(H->ev[7]));
+    float a = 0, b = 0, c = 0;
+    GOFMM_CUDA(cudaEventElapsedTime(&a, H->dtev[0], H->dtev[1]));
+    GOFMM_CUDA(cudaEventElapsedTime(&b, H->dtev[2], H->dtev[3]));
+    GOFMM_CUDA(cudaEventElapsedTime(&c, H->dtev[0], H->ev[7]));
+    if (ms3) {
+      ms3[0] = a;
+      ms3[1] = b;
+      ms3[2] = c;
+    }
+  }
+}
+
+template <class T>
+int dist_evaluate_entry(gofmm_handle* H, const T* d_w, int64_t ldw, int32_t r, T* d_u, int64_t ldu, void* stream,
+                        int32_t timed, double* ms3) {
+  return guarded([&] {
+    check_args(H, d_w, ldw, r, d_u, ldu);
+    check_precision(H, sizeof(T) == 4 ? GOFMM_PRECISION_F32 : GOFMM_PRECISION_F64);
+    std::lock_guard<std::mutex> lk(H->mu);
+    GOFMM_CUDA(cudaSetDevice(H->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    WsGuard ws(H, st);
+    dist_evaluate<T>(H, d_w, ldw, r, d_u, ldu, st, timed != 0, ms3);
+  });
+}
+}  // namespace
+
+extern "C" {
+
+int gofmm_nccl_unique_id(void* id_out) {
+  return guarded([&] {
+    if (!id_out) throw Error(GOFMM_ERR_INVALID, "null unique id buffer");
+    std::string why;
+    const nccl::Api* api = nccl::api(&why);
+    if (!api) throw Error(GOFMM_ERR_CUDA, why);
+    nccl::UniqueId id;
+    const nccl::result_t rc = api->GetUniqueId(&id);
+    if (rc != nccl::kSuccess) throw Error(GOFMM_ERR_CUDA, std::string("ncclGetUniqueId: ") + api->GetErrorString(rc));
+    std::memcpy(id_out, &id, sizeof(id));
+  });
+}
+
+int gofmm_dist_init_comm(gofmm_handle* H, const void* unique_id) {
+  return guarded([&] {
+    if (!H || !unique_id) throw Error(GOFMM_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(H->mu);
+    if (H->comm) throw Error(GOFMM_ERR_INVALID, "handle already has a communicator");
+    std::string why;
+    const nccl::Api* api = nccl::api(&why);
+    if (!api) throw Error(GOFMM_ERR_CUDA, why);
+    GOFMM_CUDA(cudaSetDevice(H->device));
+    nccl::UniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    nccl::comm_t c = nullptr;
+    const nccl::result_t rc = api->CommInitRank(&c, H->nranks, id, H->drank);
+    if (rc != nccl::kSuccess) throw Error(GOFMM_ERR_CUDA, std::string("ncclCommInitRank: ") + api->GetErrorString(rc));
+    H->comm = c;
+    H->own_comm = true;
+  });
+}
+
+int gofmm_dist_attach_comm(gofmm_handle* H, void* nccl_comm) {
+  return guarded([&] {
+    if (!H || !nccl_comm) throw Error(GOFMM_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(H->mu);
+    if (H->comm) throw Error(GOFMM_ERR_INVALID, "handle already has a communicator");
+    std::string why;
+    const nccl::Api* api = nccl::api(&why);
+    if (!api) throw Error(GOFMM_ERR_CUDA, why);
+    auto c = static_cast<nccl::comm_t>(nccl_comm);
+    int count = 0, me = 0;
+    if (api->CommCount(c, &count) != nccl::kSuccess || api->CommUserRank(c, &me) != nccl::kSuccess)
+      throw Error(GOFMM_ERR_INVALID, "not a valid NCCL communicator");
+    if (count != H->nranks || me != H->drank)
+      throw Error(GOFMM_ERR_INVALID, "communicator rank/size (" + std::to_string(me) + "/" + std::to_string(count) +
+                                         ") differ from the handle's (" + std::to_string(H->drank) + "/" +
+                                         std::to_string(H->nranks) + ")");
+    H->comm = c;
+    H->own_comm = false;
+  });
+}
+
+int gofmm_dist_evaluate(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, double* d_u, int64_t ldu,
+                        void* stream, int32_t timed, double* ms3) {
+  return dist_evaluate_entry<double>(H, d_w, ldw, r, d_u, ldu, stream, timed, ms3);
+}
+
+int gofmm_dist_evaluate_f32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, float* d_u, int64_t ldu,
+                            void* stream, int32_t timed, double* ms3) {
+  return dist_evaluate_entry<float>(H, d_w, ldw, r, d_u, ldu, stream, timed, ms3);
 }
 
 int gofmm_destroy(gofmm_handle* H) {
@@ -2047,6 +2284,10 @@ int gofmm_destroy(gofmm_handle* H) {
       if (e) cudaEventDestroy(e);
     for (auto& e : H->lev)
       if (e) cudaEventDestroy(e);
+    if (H->ws_free) {
+      cudaEventSynchronize(H->ws_free);
+      cudaEventDestroy(H->ws_free);
+    }
     if (H->stream) cudaStreamDestroy(H->stream);
     for (auto* st : {H->s_h2d, H->s_d2h})
       if (st) cudaStreamDestroy(st);
@@ -2062,6 +2303,13 @@ int gofmm_destroy(gofmm_handle* H) {
     for (auto& e : H->hpev)
       if (e) cudaEventDestroy(e);
     for (auto& e : H->upev)
+      if (e) cudaEventDestroy(e);
+    if (H->s_comm) cudaStreamSynchronize(H->s_comm);
+    if (H->comm && H->own_comm) {
+      if (const nccl::Api* api = nccl::api(nullptr)) api->CommDestroy(H->comm);
+    }
+    if (H->s_comm) cudaStreamDestroy(H->s_comm);
+    for (auto* e : {H->ev_pack, H->ev_gath, H->dtev[0], H->dtev[1], H->dtev[2], H->dtev[3]})
       if (e) cudaEventDestroy(e);
     if (H->gexec) cudaGraphExecDestroy(H->gexec);
     if (H->cap_stream) cudaStreamDestroy(H->cap_stream);
@@ -2081,6 +2329,7 @@ int gofmm_phase_flops(const gofmm_handle* H, int32_t r, int64_t* out3) {
 int gofmm_launch_profile(const gofmm_handle* H, int32_t r, int32_t cap, gofmm_launch_info* out, int32_t* count) {
   return guarded([&] {
     if (!H || !count) throw Error(GOFMM_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(H->mu);
     *count = int32_t(H->launches.size());
     for (int32_t i = 0; i < std::min<int32_t>(cap, *count); ++i) {
       const Launch& L = H->launches[i];
@@ -2122,9 +2371,12 @@ int gofmm_evaluate_device(gofmm_handle* H, const double* d_w, int64_t ldw, int32
                           void* stream, int32_t stats_sync, gofmm_eval_stats* stats) {
   return guarded([&] {
     check_args(H, d_w, ldw, r, d_u, ldu);
+    check_single(H);
+    std::lock_guard<std::mutex> lk(H->mu);
     check_precision(H, GOFMM_PRECISION_F64);
     GOFMM_CUDA(cudaSetDevice(H->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    WsGuard ws(H, st);
     auto t0 = std::chrono::steady_clock::now();
     enqueue(H, d_w, ldw, r, d_u, ldu, st, stats && stats_sync);
     if (stats) {
@@ -2152,10 +2404,13 @@ void evaluate_host(gofmm_handle* H, const T* w, int64_t ldw, int32_t r, T* u_per
   // first upload and the last download are exposed.
   constexpr bool kF32 = sizeof(T) == 4;
   check_args(H, w, ldw, r, u_perm, ldu);
+  check_single(H);
   check_precision(H, kF32 ? GOFMM_PRECISION_F32 : GOFMM_PRECISION_F64);
+  std::lock_guard<std::mutex> lk(H->mu);
   GOFMM_CUDA(cudaSetDevice(H->device));
   auto t0 = std::chrono::steady_clock::now();
   cudaStream_t st = H->stream;
+  WsGuard ws(H, st);
   if (!H->s_h2d) {
     GOFMM_CUDA(cudaStreamCreateWithFlags(&H->s_h2d, cudaStreamNonBlocking));
     GOFMM_CUDA(cudaStreamCreateWithFlags(&H->s_d2h, cudaStreamNonBlocking));
@@ -2356,9 +2611,12 @@ int gofmm_evaluate_device_f32(gofmm_handle* H, const float* d_w, int64_t ldw, in
                               void* stream, int32_t stats_sync, gofmm_eval_stats* stats) {
   return guarded([&] {
     check_args(H, d_w, ldw, r, d_u, ldu);
+    check_single(H);
+    std::lock_guard<std::mutex> lk(H->mu);
     check_precision(H, GOFMM_PRECISION_F32);
     GOFMM_CUDA(cudaSetDevice(H->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    WsGuard ws(H, st);
     auto t0 = std::chrono::steady_clock::now();
     enqueue32(H, d_w, ldw, r, d_u, ldu, st, stats && stats_sync);
     if (stats) {
@@ -2395,8 +2653,10 @@ int gofmm_exact_rows(gofmm_handle* H, const int32_t* rows, int32_t nrows, const 
       throw Error(GOFMM_ERR_INVALID, "exact rows need a matrix-free kernel source");
     if (nrows < 1 || !rows || !d_out || ldo < nrows) throw Error(GOFMM_ERR_INVALID, "exact rows: bad arguments");
     if (H->nranks > 1) throw Error(GOFMM_ERR_INVALID, "exact rows: single-GPU handles only");
+    std::lock_guard<std::mutex> lk(H->mu);
     GOFMM_CUDA(cudaSetDevice(H->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : H->stream;
+    WsGuard ws(H, st);
     const int D = H->dim;
     std::vector<double> x(size_t(nrows) * D);
     for (int i = 0; i < nrows; ++i) {
@@ -2492,8 +2752,15 @@ struct RefRng {
 
 int gofmm_rng_eps2_draw(uint64_t seed, int32_t n, int32_t r, int32_t sample_rows, int32_t* rows_out,
                         double* w_out, int64_t ldw) {
+  return gofmm_rng_eps2_draw_attempt(seed, n, r, sample_rows, 0, rows_out, w_out, ldw);
+}
+
+int gofmm_rng_eps2_draw_attempt(uint64_t seed, int32_t n, int32_t r, int32_t sample_rows, int32_t attempt,
+                                int32_t* rows_out, double* w_out, int64_t ldw) {
   return guarded([&] {
     if (n < 1 || r < 1 || sample_rows < 1) throw Error(GOFMM_ERR_INVALID, "eps2 draw: bad sizes");
+    if (attempt < 0 || attempt > 2) throw Error(GOFMM_ERR_INVALID, "eps2 draw: attempt must be 0, 1 or 2");
+    if (w_out && ldw < n) throw Error(GOFMM_ERR_INVALID, "eps2 draw: ldw < n");
     RefRng rng(seed, 0xe952);
     const int k = std::min(sample_rows, n);
     std::vector<int> out;
@@ -2510,7 +2777,10 @@ int gofmm_rng_eps2_draw(uint64_t seed, int32_t n, int32_t r, int32_t sample_rows
       }
       std::sort(out.begin(), out.end());
     }
-    std::copy(out.begin(), out.end(), rows_out);
+    if (rows_out) std::copy(out.begin(), out.end(), rows_out);
+    // evaluate.hpp:343-346: attempt a's W follows the earlier attempts' draws on the same stream
+    for (int a = 0; a < attempt; ++a)
+      for (int64_t q = 0; q < int64_t(r) * n; ++q) rng.gauss();
     if (w_out)
       for (int c = 0; c < r; ++c)
         for (int i = 0; i < n; ++i) w_out[i + size_t(c) * ldw] = rng.gauss();

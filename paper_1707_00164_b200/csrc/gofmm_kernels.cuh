@@ -43,11 +43,16 @@ struct Term {
   int32_t pad;
 };
 
+// Group flags. kGroupLoadC: the accumulator starts from the current C instead of zero, so a term
+// chain can be continued by a later launch with bitwise the same result as one launch (the
+// distributed output phase runs D + near terms before the all-gather and proj^T c after it).
+enum : int32_t { kGroupLoadC = 1 };
+
 struct Group {
   int64_t crow;  // first output row in the launch's C base (column-major, ldc given at launch)
   int32_t M;
   int32_t tbeg, tend;  // terms [tbeg, tend)
-  int32_t pad;
+  int32_t flags;       // kGroupLoadC
 };
 
 struct Tile {
@@ -504,6 +509,22 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
   for (int i = 0; i < S::MT; ++i)
 #pragma unroll
     for (int j = 0; j < S::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (grp.flags & kGroupLoadC) {  // continue a chain: same addressing as the epilogue
+#pragma unroll
+    for (int i = 0; i < S::MT; ++i) {
+      const int m = m0 + wm0 + 8 * i + g;
+      if (m >= M) continue;
+      const double* crow_ptr = cpanel ? cbase + (grp.crow >> 4) * ldc + size_t(m >> 4) * ldc + (m & 15)
+                                      : cbase + grp.crow + m;
+      const size_t cstride = cpanel ? 16 : size_t(ldc);
+#pragma unroll
+      for (int j = 0; j < S::NT; ++j) {
+        const int n = n0 + wn0 + 8 * j + 2 * tig;
+        if (n < R) acc[i][j][0] = crow_ptr[size_t(n) * cstride];
+        if (n + 1 < R) acc[i][j][1] = crow_ptr[size_t(n + 1) * cstride];
+      }
+    }
+  }
 
   // swizzled B fragment offsets: row n = wn0 + 8j + g has (n & 7) == g
   uint32_t boff[kBK / 4];

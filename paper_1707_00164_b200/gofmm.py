@@ -129,13 +129,20 @@ def make_desc(tree: CompressedTree, stored: bool | None = None):
     return d, keep, use_stored
 
 
-def rng_eps2_draw(seed: int, n: int, r: int, sample_rows: int):
-    """error_eps2's draws from the reference Rng (evaluate.hpp:336-346): (rows, W)."""
+def rng_eps2_draw(seed: int, n: int, r: int, sample_rows: int, attempt: int = 0):
+    """error_eps2's draws from the reference Rng (evaluate.hpp:336-346): (rows, W of `attempt`)."""
     k = min(sample_rows, n)
     rows = np.empty(k, dtype=np.int32)
     w = np.empty((n, r), dtype=np.float64, order="F")
-    L.check(L.lib().gofmm_rng_eps2_draw(seed, n, r, sample_rows, _p(rows), _p(w), n))
+    L.check(L.lib().gofmm_rng_eps2_draw_attempt(seed, n, r, sample_rows, attempt, _p(rows), _p(w), n))
     return rows, w
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library's NCCL (rank 0 calls it; the caller broadcasts it)."""
+    buf = C.create_string_buffer(128)
+    L.check(L.lib().gofmm_nccl_unique_id(buf))
+    return buf.raw
 
 
 def dist_plan_host(tree: CompressedTree, rank: int, nranks: int) -> tuple[dict, list[int]]:
@@ -267,10 +274,16 @@ class Evaluator:
         tdt = torch.float64 if self.precision == "fp64" else torch.float32
         if not (w.is_cuda and w.dtype == tdt):
             raise L.InvalidArgument(L.GOFMM_ERR_INVALID, f"evaluate_torch: w must be a CUDA {tdt} tensor")
+        if w.dim() != 2 or w.shape[0] != self.n:  # evaluate.hpp:288
+            raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "evaluate: w has wrong row count")
+        if w.shape[1] < 1:  # evaluate.hpp:289
+            raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "evaluate: w needs at least one column")
         wt = _colmajor(w)
         r = int(w.shape[1])
         if out is None:
             out = torch.empty((r, self.n), dtype=tdt, device=w.device).t()
+        else:
+            _check_out(out, self.n, r, tdt, w.device)
         stream = torch.cuda.current_stream(w.device).cuda_stream
         stats = self.evaluate_device(wt.data_ptr(), wt.stride(1), r, out.data_ptr(), out.stride(1), stream,
                                      sync_stats)
@@ -307,6 +320,35 @@ class Evaluator:
                                           C.c_void_p(out.data_ptr()), out.stride(1),
                                           C.c_void_p(stream if stream else 1)))
 
+    def init_comm(self, unique_id: bytes):
+        """Create the library-owned NCCL communicator of this rank (collective over all ranks)."""
+        if len(unique_id) != 128:
+            raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "unique id must be 128 bytes")
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        L.check(L.lib().gofmm_dist_init_comm(self._h, buf))
+
+    def attach_comm(self, comm_ptr: int):
+        """Borrow an existing ncclComm_t (e.g. ProcessGroupNCCL._comm_ptr()) of the same NCCL."""
+        L.check(L.lib().gofmm_dist_attach_comm(self._h, C.c_void_p(comm_ptr)))
+
+    def dist_evaluate_torch(self, w, out, timed: bool = False) -> dict | None:
+        """One distributed evaluation on the library's own data plane (stage 1 -> ncclAllGather ->
+        stage 2, the own D + near output terms overlapping the all-gather); writes this rank's rows
+        of u_perm into `out`. timed: {stage1_ms, allgather_ms, total_ms} (synchronises)."""
+        import torch
+
+        if w.dim() != 2 or w.shape[0] != self.n or w.shape[1] < 1:
+            raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "evaluate: w has wrong shape")
+        wt = _colmajor(w)
+        r = int(w.shape[1])
+        _check_out(out, self.n, r, wt.dtype, w.device)
+        stream = torch.cuda.current_stream(w.device).cuda_stream
+        ms = (C.c_double * 3)()
+        fn = L.lib().gofmm_dist_evaluate if self.precision == "fp64" else L.lib().gofmm_dist_evaluate_f32
+        L.check(fn(self._h, C.c_void_p(wt.data_ptr()), wt.stride(1), r, C.c_void_p(out.data_ptr()), out.stride(1),
+                   C.c_void_p(stream if stream else 1), 1 if timed else 0, ms))
+        return dict(stage1_ms=ms[0], allgather_ms=ms[1], total_ms=ms[2]) if timed else None
+
     def evaluate_dist_torch(self, w, out, all_gather):
         """One distributed evaluation: stage1, all_gather(send) -> recv, stage2. `all_gather` maps
         this rank's flat send tensor to the rank-ordered concatenation of every rank's."""
@@ -341,18 +383,22 @@ class Evaluator:
             raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "sample_rows must be >= 1")
         if r < 1:
             raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "r must be >= 1")
-        rows, w = rng_eps2_draw(seed, self.n, r, sample_rows)
-        pot = self.evaluate(w)
-        u = self.unpermute(pot.u)[rows]
-        exact = self.exact_rows(rows, w)
-        dn = np.linalg.norm(u - exact, axis=1)
-        de = np.linalg.norm(exact, axis=1)
-        num, den = float((dn ** 2).sum()), float((de ** 2).sum())
-        if den == 0.0:  # the reference redraws W up to 3 times (evaluate.hpp:343-372)
-            raise L.GofmmError(L.GOFMM_ERR_NUMERIC, "error_eps2: sampled rows of Kw vanished")
-        rel = np.where(de > 0, dn / np.where(de > 0, de, 1.0), 0.0)
-        return dict(eps2=float(np.sqrt(num / den)), per_entry=rel[:10].tolist(), mean_sample=float(rel.mean()),
-                    sample_rows=rows.tolist(), eval_flops=pot.flops, eval_seconds=pot.seconds)
+        # the reference redraws W from the same Rng stream up to 3 times while the sampled rows
+        # of K w vanish (evaluate.hpp:343-372); attempt a's W continues that stream
+        for attempt in range(3):
+            rows, w = rng_eps2_draw(seed, self.n, r, sample_rows, attempt)
+            pot = self.evaluate(w)
+            u = self.unpermute(pot.u)[rows]
+            exact = self.exact_rows(rows, w)
+            dn = np.linalg.norm(u - exact, axis=1)
+            de = np.linalg.norm(exact, axis=1)
+            num, den = float((dn ** 2).sum()), float((de ** 2).sum())
+            if den == 0.0:
+                continue
+            rel = np.where(de > 0, dn / np.where(de > 0, de, 1.0), 0.0)
+            return dict(eps2=float(np.sqrt(num / den)), per_entry=rel[:10].tolist(), mean_sample=float(rel.mean()),
+                        sample_rows=rows.tolist(), eval_flops=pot.flops, eval_seconds=pot.seconds)
+        raise L.GofmmError(L.GOFMM_ERR_NUMERIC, "error_eps2: sampled rows of Kw vanished repeatedly")
 
     def unpermute(self, u_perm: np.ndarray) -> np.ndarray:
         """out.row(iperm[t]) = u_perm.row(t) (evaluate.hpp:21-25)."""
@@ -360,6 +406,20 @@ class Evaluator:
         out = np.empty_like(u_perm)
         out[np.asarray(self.tree.iperm, dtype=np.int64)] = u_perm
         return out
+
+
+def _check_out(out, n: int, r: int, dtype, device) -> None:
+    """A caller-supplied device output must be exactly what the kernels write: N x r, the handle's
+    dtype, on w's device, column-major (stride(0) == 1, stride(1) >= N) — else the C side, which
+    only sees a pointer and ldu, would write past the tensor."""
+    if out.dim() != 2 or tuple(out.shape) != (n, r):
+        raise L.InvalidArgument(L.GOFMM_ERR_INVALID, f"out must be {n} x {r}, got {tuple(out.shape)}")
+    if out.dtype != dtype:
+        raise L.InvalidArgument(L.GOFMM_ERR_INVALID, f"out must be {dtype}, got {out.dtype}")
+    if out.device != device:
+        raise L.InvalidArgument(L.GOFMM_ERR_INVALID, f"out must be on {device}, got {out.device}")
+    if out.stride(0) != 1 or (r > 1 and out.stride(1) < n):
+        raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "out must be column-major (stride(0) == 1, stride(1) >= N)")
 
 
 def _colmajor(t):

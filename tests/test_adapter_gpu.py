@@ -1,8 +1,11 @@
 """The header-only C++ adapter (include/gofmm_b200_gfmm.hpp) over the reference API, compiled with
 the reference headers into oracle/_ref/adapter_test (oracle/Makefile, target `adapter`): the
-reference's own compress() + evaluate() next to gfmm::B200Evaluator on the same HMatrix —
-stored-block and matrix-free GPU results within 1e-12, equal flop counters, and
-std::invalid_argument on a wrong-sized W (evaluate.hpp:288-289)."""
+reference's own compress() + evaluate() + error_eps2() next to the adapter on the same HMatrix —
+gfmm::evaluate_b200(h, w, opts) (evaluate()'s signature, cached per HMatrix), the stored and the
+matrix-free evaluators (Gaussian, Laplace, Exponential) within 1e-12 with equal flop counters,
+error_eps2_b200 == error_eps2, 4 threads calling evaluate_b200 on one HMatrix concurrently
+bitwise equal to serial calls, and std::invalid_argument on a wrong-sized W
+(evaluate.hpp:288-289)."""
 import os
 import subprocess
 

@@ -3,8 +3,9 @@
 a work-balanced contiguous run of the subtrees up to two levels below log2(P);
 the ranks all-gather their plans and check, against an independent Python restatement, that
 (1) the owned row ranges partition [0, N); (2) every ghost a rank needs (what of cross-subtree
-far partners and of all split-level nodes, W rows of cross-subtree near partners) is exported by
-its owner; (3) the all-gather slot size agrees on every rank."""
+far partners and of all split-level nodes) is exported by its owner, and nothing else is: W is
+replicated, so W rows of cross-subtree near partners never travel, and every exported what is
+needed by at least one other rank; (3) the all-gather slot size agrees on every rank."""
 import os
 import socket
 
@@ -69,7 +70,12 @@ def _worker(rank, world, port, q):
             exported_what |= {e for e in exp if e >= 0}
             exported_w |= {-e - 1 for e in exp if e < 0}
         assert need_what <= exported_what, sorted(need_what - exported_what)[:10]
-        assert need_w <= exported_w, sorted(need_w - exported_w)[:10]
+        assert not exported_w, "W rows are replicated and must not be exported"
+        # no redundant export: every what this rank exports is needed by some other rank
+        needs_by_rank = [independent_needs(tree, h, info["split_level"], ranges_by_rank)[1] for h in range(world)]
+        wanted = set().union(*[needs_by_rank[h] for h in range(world) if h != rank])
+        mine = {e for e in ids if e >= 0}
+        assert mine <= wanted, sorted(mine - wanted)[:10]
         assert len({p[0]["max_send_rows"] for p in plans}) == 1
         ranges = sorted((p[0]["own_row_begin"], p[0]["own_row_end"]) for p in plans)
         assert ranges[0][0] == 0 and ranges[-1][1] == tree.n
