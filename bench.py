@@ -9,10 +9,12 @@ format). Inputs (W, 4.3 GB) exceed L2 (126 MB), so no extra flush is needed betw
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
 
 Under torchrun (N > 1, N a power of two) the SAME config-3 evaluation is split across the ranks
-(strong scaling): the tree is cut at level log2(N), rank g owns the g-th subtree, nodes above the
-cut are evaluated redundantly, and one NCCL all-gather per evaluation exchanges the skeleton
-weights and W rows other ranks need (north_star (4)). The timed region is bracketed
-by a barrier + synchronize and the max over ranks is used.
+(strong scaling): the tree is cut at level log2(N) (+ up to 3 for balance), each rank owns a
+contiguous run of subtrees, nodes above the cut are evaluated redundantly, and one NCCL all-gather
+per evaluation — issued by the library itself (gofmm_dist_evaluate) on an NCCL communicator it
+creates from a broadcast unique id — exchanges the skeleton weights other ranks need (W is
+replicated), overlapped with the own leaves' D + near output terms (north_star (4)).
+The timed region is bracketed by a barrier + synchronize and the max over ranks is used.
 """
 from __future__ import annotations
 
@@ -126,6 +128,9 @@ def dist_setup():
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # NCCL's init lines (rank count, NVLink / NVLS transport) on stderr for the run log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
     return world, rank, local
 
@@ -149,30 +154,64 @@ def allmax(x: float, world: int) -> float:
 
 
 # ------------------------------------------------------------------ CPU reference (oracle) legs
+def host_info() -> dict:
+    """The host the CPU legs run on: lscpu model, usable cores, memory (free -g)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                info["cpu_model"] = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        with open("/proc/meminfo") as f:
+            mem = {ln.split(":")[0]: int(ln.split()[1]) for ln in f if ln.split()}
+        info["mem_total_gb"] = round(mem["MemTotal"] / 2 ** 20, 1)
+        info["mem_available_gb"] = round(mem["MemAvailable"] / 2 ** 20, 1)
+    except Exception:
+        pass
+    return info
+
+
 def cpu_sample_tree(cfg: dict, n_sample: int, seed: int):
     """A bounded sample of the workload: a c3-shaped tree (same d, m, s, budget, kernel) on
-    n_sample points, imported into the reference HMatrix through the reference oracle."""
+    n_sample points — the SAME tree for the reference arm, the cpu_baseline leg and the GPU's
+    same-config leg."""
     from paper_1707_00164_b200 import synth
 
     tree, _ = synth.make_config_tree(cfg["name"], seed=seed, n=n_sample, budget=cfg["budget"])
     return tree
 
 
-def run_reference_sample(tree, r: int, reps: int, threads: int):
-    """Time the reference's own evaluate() (oracle/_ref: reference headers, unmodified) on the host."""
+def sample_rhs(n: int, r: int) -> np.ndarray:
+    return np.asfortranarray(np.random.default_rng(1).standard_normal((n, r)))
+
+
+def cpu_protocol(ref, w: np.ndarray, threads: int, reps: int, warmup: int) -> dict:
+    """THE CPU timing protocol of both CPU legs (reference arm and cpu_baseline): the reference
+    gfmm::evaluate (oracle/_ref, unmodified headers) in both executors — TaskDag (EvalOptions'
+    default, evaluate.hpp:122-126) and LevelByLevel (evaluate.hpp:222-235) — `warmup` untimed
+    runs each, then the median of `reps` Potentials.seconds per mode. value = TaskDag."""
     from oracle import refpy as R
 
-    ref = R.import_flat(tree, threads=threads)
-    w = np.asfortranarray(np.random.default_rng(1).standard_normal((tree.n, r)))
-    times, flops, u = [], 0, None
-    for _ in range(reps):
-        u, flops, sec = ref.evaluate(w, mode=R.TASK_DAG, threads=threads)
-        times.append(sec)
-    return dict(ref=ref, w=w, u=u, flops=flops, times=times)
+    out, flops, u = {}, 0, None
+    for name, mode in (("task_dag", R.TASK_DAG), ("level_by_level", R.LEVEL_BY_LEVEL)):
+        for _ in range(warmup):
+            ref.evaluate(w, mode=mode, threads=threads)
+        secs = []
+        for _ in range(reps):
+            u, flops, sec = ref.evaluate(w, mode=mode, threads=threads)
+            secs.append(sec)
+        out[name] = {"median_s": float(np.median(secs)), "runs_s": [round(x, 4) for x in secs]}
+    out["flops"] = int(flops)
+    out["u"] = u
+    return out
 
 
 def reference_arm(args, world, rank):
-    """--impl reference: the reference CPU evaluate on this box's host cores."""
+    """--impl reference: the reference CPU evaluate on this box's host cores (cpu_protocol with
+    reps = --steps, warmup = --warmup, on the bounded c3-shaped sample)."""
     if rank != 0:
         return 0
     from paper_1707_00164_b200 import synth
@@ -185,28 +224,66 @@ def reference_arm(args, world, rank):
     from oracle import refpy as R
 
     ref = R.import_flat(tree, threads=threads)
-    w = np.asfortranarray(np.random.default_rng(1).standard_normal((tree.n, r)))
-    for _ in range(args.warmup):
-        ref.evaluate(w, mode=R.TASK_DAG, threads=threads)
-    secs, flops = [], 0
-    for _ in range(args.steps):
-        _, flops, sec = ref.evaluate(w, mode=R.TASK_DAG, threads=threads)
-        secs.append(sec)
-    ms = 1e3 * float(np.mean(secs))
-    val = flops / (ms * 1e-3) / 1e9
-    sample = (f"{args.config}-shaped tree at N={tree.n} (same d/m/s/budget/kernel), r={r}; reference "
-              f"gfmm::evaluate (TaskDag) per step, Potentials.seconds")
+    w = sample_rhs(tree.n, r)
+    res = cpu_protocol(ref, w, threads, reps=max(args.steps, 3), warmup=max(args.warmup, 1))
+    sec = res["task_dag"]["median_s"]
+    val = res["flops"] / sec / 1e9
+    sample = (f"{args.config}-shaped tree at N={tree.n} (same d/m/s/budget/kernel, synth.py seed {args.seed}), "
+              f"r={r}; reference gfmm::evaluate, TaskDag x{threads} threads, median of {max(args.steps, 3)} "
+              f"Potentials.seconds after {max(args.warmup, 1)} warm-up")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "GFLOP/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sec, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config} sample N={tree.n} r={r}", "n": tree.n, "r": r, "cpu_threads": threads},
         "cpu_baseline": {"value": round(val, 3), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "sample": sample,
+                         "level_by_level_gflops": round(res["flops"] / res["level_by_level"]["median_s"] / 1e9, 3),
+                         "runs_s": res["task_dag"]["runs_s"], "host": host_info()},
         "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def same_config_leg(ev_cls, tree, w: np.ndarray, precision: str, local: int, reps: int = 5) -> dict:
+    """The GPU on exactly the reference arm's tree and W: device-resident (CUDA events, median of
+    `reps` after a warm-up, L2 flushed before each) and end to end through the host API
+    (gofmm_evaluate with pinned host buffers, median of `reps` wall times)."""
+    import torch
+
+    tdt = torch.float32 if precision == "fp32" else torch.float64
+    ndt = np.float32 if precision == "fp32" else np.float64
+    with ev_cls(tree, device=local, precision=precision) as es:
+        flops = es.flops(w.shape[1])
+        wd = torch.from_numpy(np.ascontiguousarray(w.T.astype(ndt))).cuda().t()
+        ud = torch.empty_like(wd.t()).t()
+        flush = torch.empty(256 * 2 ** 20 // 8, dtype=torch.float64, device="cuda")
+        es.evaluate_torch(wd, out=ud)
+        st = torch.cuda.current_stream()
+        ms = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            es.evaluate_torch(wd, out=ud)
+            b.record(st)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        wh = torch.empty((w.shape[1], w.shape[0]), dtype=tdt, pin_memory=True)
+        wh.copy_(torch.from_numpy(np.ascontiguousarray(w.T.astype(ndt))))
+        uh = torch.empty_like(wh).pin_memory()
+        wn, un = wh.numpy().T, uh.numpy().T
+        es.evaluate(wn, out=un)
+        ts = []
+        for _ in range(reps):
+            t1 = time.perf_counter()
+            p = es.evaluate(wn, out=un)
+            ts.append(time.perf_counter() - t1)
+        u = un.astype(np.float64)
+    dev_s, e2e_s = float(np.median(ms)) / 1e3, float(np.median(ts))
+    return {"flops": int(flops), "device_s": dev_s, "e2e_s": e2e_s, "u": u,
+            "device_gflops": flops / dev_s / 1e9, "e2e_gflops": flops / e2e_s / 1e9}
 
 
 KERNEL_NAMES = {0: "Gaussian", 1: "Laplace", 2: "Polynomial", 4: "Exponential (Matern-1/2)"}
@@ -324,24 +401,39 @@ def ours_arm(args, world, rank, local):
                "ms_d2h": round(p.stats["ms_d2h"], 3)}
         del w_h, u_h
 
-    # CPU baseline (reference evaluate on a bounded sample) + parity of the GPU on that sample
-    cpu = None
-    rel_err = None
+    # CPU baseline (reference evaluate on a bounded sample, the reference arm's protocol) + the GPU
+    # on exactly that tree and W (same-config ratio) + parity of the GPU on that tree
+    cpu, same, rel_err = None, None, None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
+            from oracle import refpy as R
+
             cfg_s = dict(cfg)
             cfg_s["name"] = args.config
             stree = cpu_sample_tree(cfg_s, min(args.cpu_n, tree.n), seed=args.seed)
             threads = os.cpu_count() or 1
-            res = run_reference_sample(stree, r, reps=2, threads=threads)
-            cpu_sec = float(np.median(res["times"]))
-            cpu = {"value": round(res["flops"] / cpu_sec / 1e9, 3), "unit": "GFLOP/s", "cores": threads,
-                   "kind": "reference",
-                   "sample": f"{args.config}-shaped tree at N={stree.n} (same d/m/s/budget/kernel), r={r}, "
-                             f"reference gfmm::evaluate TaskDag x{threads} threads, median of 2 Potentials.seconds"}
-            with Evaluator(stree, device=local, precision=args.precision) as es:
-                pu = es.evaluate(res["w"])
-            rel_err = float(np.linalg.norm(pu.u.astype(np.float64) - res["u"]) / np.linalg.norm(res["u"]))
+            ws = sample_rhs(stree.n, r)
+            ref = R.import_flat(stree, threads=threads)
+            res = cpu_protocol(ref, ws, threads, reps=3, warmup=1)
+            del ref
+            cpu_sec = res["task_dag"]["median_s"]
+            cpu_val = res["flops"] / cpu_sec / 1e9
+            cpu = {"value": round(cpu_val, 3), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
+                   "sample": f"{args.config}-shaped tree at N={stree.n} (same d/m/s/budget/kernel, synth.py seed "
+                             f"{args.seed}), r={r}; reference gfmm::evaluate, TaskDag x{threads} threads, median of 3 "
+                             f"Potentials.seconds after 1 warm-up (the reference arm's protocol)",
+                   "level_by_level_gflops": round(res["flops"] / res["level_by_level"]["median_s"] / 1e9, 3),
+                   "runs_s": res["task_dag"]["runs_s"], "host": host_info()}
+            sc = same_config_leg(Evaluator, stree, ws, args.precision, local)
+            rel_err = float(np.linalg.norm(sc["u"] - res["u"]) / np.linalg.norm(res["u"]))
+            same = {"tree": cpu["sample"].split(";")[0], "r": r, "flops": sc["flops"],
+                    "gpu_device_gflops": round(sc["device_gflops"], 3), "gpu_e2e_gflops": round(sc["e2e_gflops"], 3),
+                    "reference_gflops": round(cpu_val, 3),
+                    "ratio_device": round(sc["device_gflops"] / cpu_val, 2),
+                    "ratio_e2e": round(sc["e2e_gflops"] / cpu_val, 2),
+                    "rel_error_vs_reference": rel_err,
+                    "note": "GPU timed on the reference arm's exact tree and W (device: CUDA events, L2 flushed, "
+                            "median of 5; e2e: gofmm_evaluate with pinned host buffers, median of 5)"}
         except Exception as exc:  # report, never hide
             cpu = {"value": None, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {exc!r}"[:300]}
@@ -362,12 +454,14 @@ def ours_arm(args, world, rank, local):
         ("pct_3xtf32_peak" if f32 else "pct_fp64_peak"): round(100.0 * value / 1e3 / (peak * world), 2),
         "flops_per_eval": int(flops),
         "rel_error": rel_err,
+        "rel_error_tree": (same or {}).get("tree"),
         "phase_ms": {k: round(v[1], 3) for k, v in phases.items()} | {"permute": round(ph["ms_permute"], 3)},
         "roofline": {"bound": "tensor", "kernel": dom_name, "achieved": round(achieved, 3),
                      "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "peak_source": peak_src, "launch_ms": round(dom["ms"], 3), "launch_flops": int(dom["flops"]),
                      "share_of_step": round(dom["ms"] / ms, 4)},
         "cpu_baseline": cpu,
+        "same_config": same,
         "e2e": e2e,
         "gpu_launches": int(ev.launches_per_eval * args.steps),
         "setup_s": {"tree_gen": round(t_gen, 2), "create_upload": round(t_create, 2)},
@@ -387,7 +481,7 @@ def dist_arm(args, world, rank, local):
     import torch
     import torch.distributed as dist
 
-    from paper_1707_00164_b200 import Evaluator, synth
+    from paper_1707_00164_b200 import Evaluator, gofmm, synth
 
     torch.cuda.set_device(local)
     cfg = dict(synth.CONFIGS[args.config])
@@ -411,14 +505,16 @@ def dist_arm(args, world, rank, local):
     w = torch.randn((r, tree.n), dtype=tdt, device="cuda", generator=gen).t()
     u = torch.zeros((r, tree.n), dtype=tdt, device="cuda").t()
     slot = ev.send_elems(r)
-    send = torch.empty(slot, dtype=tdt, device="cuda")
-    recv = torch.empty(slot * world, dtype=tdt, device="cuda")
+    if world > 1:
+        # the library's own data plane: an NCCL communicator created from a unique id that rank 0
+        # draws and torch.distributed broadcasts; one ncclAllGather per evaluation inside
+        # gofmm_dist_evaluate, overlapped with the own leaves' D + near output terms
+        uid = [gofmm.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ev.init_comm(uid[0])
 
     def step():
-        ev.dist_stage1_torch(w, send)
-        if slot and world > 1:
-            dist.all_gather_into_tensor(recv, send)
-        ev.dist_stage2_torch(recv, r, u)
+        ev.dist_evaluate_torch(w, u)
 
     for _ in range(args.warmup):
         step()
@@ -437,6 +533,11 @@ def dist_arm(args, world, rank, local):
     ms = allmax(e0.elapsed_time(e1) / args.steps, world)
     value = full_flops / (ms * 1e-3) / 1e9
     peak, peak_src = tf32x3_peak_tflops() if f32 else fp64_peak_tflops()
+    # one more evaluation with the library's event timing: stage 1 and the all-gather (on its own
+    # stream, overlapping the own D + near output terms), max over ranks
+    barrier(world)
+    tm = ev.dist_evaluate_torch(w, u, timed=True)
+    exchange = {k: round(allmax(v, world), 3) for k, v in tm.items()}
 
     # zero-communication baseline: the whole tree replicated on every GPU, each
     # evaluating r / N of the columns (evaluation is column-separable)
@@ -491,6 +592,7 @@ def dist_arm(args, world, rank, local):
                                f"d={cfg['d']} m={cfg['m']} s={cfg['s']} budget={cfg['budget']} r={r} total",
                    "n": tree.n, "r": r, "budget": cfg["budget"], "parallelism": f"subtree split x{world}",
                    "split_level": info["split_level"], "allgather_bytes_per_rank": int(slot * esz),
+                   "exchange": "in-library ncclAllGather (gofmm_dist_evaluate), W replicated, what only",
                    "l2_flush": f"inputs larger than L2 (W {tree.n * r * esz / 1e9:.2f} GB)",
                    "precision": args.precision},
         "sec_per_eval": round(ms / 1e3, 6),
@@ -507,6 +609,7 @@ def dist_arm(args, world, rank, local):
                      "traffic": None, "peak_source": peak_src},
         "cpu_baseline": None,
         "rhs_shard_baseline": rhs_shard,
+        "exchange_ms": exchange,
         "e2e": e2e,
         "gpu_launches": int((ev.launches_per_eval + 2) * args.steps),
         "setup_s": {"tree_gen": round(t_gen, 2), "create_upload": round(t_create, 2)},
