@@ -293,6 +293,62 @@ int gofmm_ann_leaf_merge(int32_t n, int32_t d, const double* coords, int32_t kin
                          int32_t* table_j, double* table_d, int32_t* table_len, double* kernel_ms);
 const char* gofmm_ann_last_error(void);
 
+/* ---- compress: the input of gofmm_create from a point cloud ---------------
+ * gfmm::compress (compress.hpp:331-434) with its kernel oracle, metric, ANN search, metric tree,
+ * near-field selection, structure walk, column sampling and skeletonisation: host pipeline with
+ * the ANN leaf passes, the per-level sampled blocks and the per-level batched CPQR / ID on the
+ * GPU. D / near / far blocks are not stored (gofmm_create regenerates them matrix-free); their
+ * entries are counted as the reference's CountingOracle counts them.
+ * entries = GOFMM_ENTRIES_HOST: every entry that steers a decision is computed on the host with
+ * the reference's formulas and reduction order -> tree, neighbour lists, skeletons, proj and all
+ * statistics bit-identical to the reference compress. GOFMM_ENTRIES_DEVICE: ANN leaf passes
+ * (geometric, or kernel L2 over a Gaussian) and sampled blocks generated on the GPU (libdevice
+ * exp/pow: a few ulps from glibc, so exact near-ties may resolve differently). */
+#define GOFMM_DIST_GEOMETRIC 0 /* DistanceKind::GeometricL2 (metric.hpp:8) */
+#define GOFMM_DIST_KERNEL 1    /* DistanceKind::KernelL2 (the reference default) */
+#define GOFMM_DIST_ANGLE 2     /* DistanceKind::Angle */
+#define GOFMM_ENTRIES_HOST 0
+#define GOFMM_ENTRIES_DEVICE 1
+
+typedef struct gofmm_compress_config { /* RunConfig (compress.hpp:12-34) + device knobs */
+  int32_t m, s;
+  double tau;
+  int32_t kappa;
+  double budget;
+  int32_t distance; /* GOFMM_DIST_* */
+  uint64_t seed;
+  int32_t ann_iterations;
+  int32_t threads; /* host threads */
+  int32_t entries; /* GOFMM_ENTRIES_* */
+  int32_t device;
+} gofmm_compress_config;
+
+typedef struct gofmm_compress_stats { /* CompressStats (compress.hpp:49-59) + structure sizes */
+  int64_t entries_evaluated, compress_flops, near_field_entries;
+  int32_t max_skeleton, ann_iterations_done;
+  double mean_skeleton, compress_seconds, tree_seconds;
+  double ann_recall[64]; /* per ANN iteration (first ann_iterations_done) */
+  double ann_seconds, ann_kernel_ms, skeleton_seconds, skel_kernel_ms;
+  int32_t depth, num_nodes, num_leaves, reserved;
+  int64_t num_near, num_far;
+} gofmm_compress_stats;
+
+typedef struct gofmm_compressed gofmm_compressed;
+
+/* RunConfig defaults (m = s = 256, tau 1e-5, kappa 32, budget 0.03, kernel distance, seed 0,
+ * 10 ANN iterations), all host threads, device entries, device 0. */
+void gofmm_compress_default_config(gofmm_compress_config* cfg);
+/* kernel: GOFMM_KERNEL_*; kparam[0..1] as gofmm_tree_desc::kparam (Laplace: the resolved floor);
+ * coords d x n column-major, original order (copied). */
+int gofmm_compress(int32_t kernel, const double* kparam, int32_t dim, int32_t n, const double* coords,
+                   const gofmm_compress_config* cfg, gofmm_compressed** out);
+/* The flattened HMatrix as a gofmm_tree_desc (GOFMM_SOURCE_KERNEL); pointers stay valid until
+ * gofmm_compressed_free. */
+int gofmm_compressed_desc(const gofmm_compressed* c, gofmm_tree_desc* desc);
+int gofmm_compressed_stats(const gofmm_compressed* c, gofmm_compress_stats* stats);
+int gofmm_compressed_free(gofmm_compressed* c);
+const char* gofmm_compress_last_error(void);
+
 /* Bytes of device memory held by the handle (tree + workspace). */
 int64_t gofmm_device_bytes(const gofmm_handle* h);
 

@@ -9,10 +9,11 @@ from ._lib import (BLOCKS_MATERIALIZE, BLOCKS_MATRIX_FREE, GOFMM_ERR_CUDA, GOFMM
 from .gofmm import CompressedTree, Evaluator, Potentials
 from .ann import ann_leaf_merge
 from .skeleton import Skeleton, skeletonize_batch
+from .compress import CompressResult, compress
 
 __all__ = [
     "BLOCKS_MATERIALIZE", "BLOCKS_MATRIX_FREE", "GOFMM_ERR_CUDA", "GOFMM_ERR_INVALID", "GOFMM_ERR_IO",
     "GOFMM_ERR_NUMERIC", "KERNEL_EXPONENTIAL", "KERNEL_GAUSSIAN", "KERNEL_LAPLACE", "KERNEL_POLYNOMIAL",
     "GofmmError", "InvalidArgument", "build", "CompressedTree", "Evaluator", "Potentials", "Skeleton",
-    "skeletonize_batch", "ann_leaf_merge",
+    "skeletonize_batch", "ann_leaf_merge", "compress", "CompressResult",
 ]

@@ -33,11 +33,12 @@ PRECISION_F32 = 1
 BLOCKS_MATRIX_FREE = 0
 BLOCKS_MATERIALIZE = 1
 
+# host code: no FP contraction (the compress pipeline reproduces the reference's SSE2 rounding)
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC"]
+              "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off"]
 # translation units of the library, compiled in parallel then linked: the C-ABI + FP64 DMMA
 # kernels, the FP32 3xTF32 tcgen05 kernels, and the compress-side batched skeletonisation and ANN pass
-UNITS = ("gofmm_capi.cu", "gofmm_f32.cu", "gofmm_skel.cu", "gofmm_ann.cu")
+UNITS = ("gofmm_capi.cu", "gofmm_f32.cu", "gofmm_skel.cu", "gofmm_ann.cu", "gofmm_compress.cu")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -135,7 +136,9 @@ EXPORTS = ("gofmm_create", "gofmm_evaluate", "gofmm_evaluate_device", "gofmm_unp
            "gofmm_unpermute_device_f32", "gofmm_precision", "gofmm_dist_stage1_f32", "gofmm_dist_stage2_f32",
            "gofmm_skeletonize_batch", "gofmm_skeletonize_last_error", "gofmm_ann_leaf_merge",
            "gofmm_ann_last_error", "gofmm_rng_eps2_draw_attempt", "gofmm_nccl_unique_id", "gofmm_dist_init_comm",
-           "gofmm_dist_attach_comm", "gofmm_dist_evaluate", "gofmm_dist_evaluate_f32")
+           "gofmm_dist_attach_comm", "gofmm_dist_evaluate", "gofmm_dist_evaluate_f32", "gofmm_compress_default_config",
+           "gofmm_compress", "gofmm_compressed_desc", "gofmm_compressed_stats", "gofmm_compressed_free",
+           "gofmm_compress_last_error")
 
 
 class SkelStats(C.Structure):

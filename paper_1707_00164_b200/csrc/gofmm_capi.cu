@@ -40,6 +40,7 @@
 #include "../../include/gofmm_b200.h"
 #include "gofmm_kernels.cuh"
 #include "gofmm_kernels_f32.cuh"
+#include "gofmm_rng.h"
 #include "nccl_dyn.h"
 
 namespace gofmm {
@@ -2719,36 +2720,6 @@ int gofmm_exact_rows(gofmm_handle* H, const int32_t* rows, int32_t nrows, const 
 // The reference Rng (common.hpp:40-104): splitmix64 stream, Box-Muller gauss with cached spare,
 // sorted rejection sample. Host code: error_eps2 draws its rows and W from it
 // (evaluate.hpp:336-346), so reproducing eps2 needs the identical stream.
-namespace {
-struct RefRng {
-  uint64_t state;
-  bool have_spare = false;
-  double spare = 0.0;
-  static uint64_t mix(uint64_t x) {
-    x += 0x9e3779b97f4a7c15ULL;
-    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
-    return x ^ (x >> 31);
-  }
-  RefRng(uint64_t seed, uint64_t stream) : state(mix(seed ^ mix(stream + 0x632be59bd9b4e019ULL))) {}
-  uint64_t next() { return state = mix(state); }
-  int uniform(int n) { return int(next() % uint64_t(n)); }
-  double uniform01() { return double(next() >> 11) * 0x1.0p-53; }
-  double gauss() {
-    if (have_spare) {
-      have_spare = false;
-      return spare;
-    }
-    double u1 = uniform01(), u2 = uniform01();
-    while (u1 <= 1e-300) u1 = uniform01();
-    double rr = std::sqrt(-2.0 * std::log(u1));
-    double a = 2.0 * M_PI * u2;
-    spare = rr * std::sin(a);
-    have_spare = true;
-    return rr * std::cos(a);
-  }
-};
-}  // namespace
 
 int gofmm_rng_eps2_draw(uint64_t seed, int32_t n, int32_t r, int32_t sample_rows, int32_t* rows_out,
                         double* w_out, int64_t ldw) {

@@ -22,21 +22,16 @@
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
+#include <string>
 #include <vector>
 
 #include "../../include/gofmm_b200.h"
+#include "gofmm_skel_internal.h"
 
 namespace gofmm_skel {
 
 constexpr int kThreads = 128;  // 3 CTAs (nodes) per SM: one node's serial pivot phase overlaps the others' streaming
 
-struct NodeDesc {
-  int64_t in_off;    // block (column-major rows x cols) in the input blob
-  int64_t ws_off;    // row-major workspace
-  int64_t perm_off;  // cols ints
-  int64_t proj_off;  // maxrank * cols doubles (written rank x cols column-major, ld = rank)
-  int32_t rows, cols;
-};
 
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
@@ -128,6 +123,7 @@ __global__ void __launch_bounds__(kThreads, 3) skeletonize_kernel(const NodeDesc
                                                                int32_t s_max, double tau_tol,
                                                                int32_t* __restrict__ rank_out,
                                                                double* __restrict__ achieved_out,
+                                                               double* __restrict__ lead_out,
                                                                int32_t* __restrict__ perm_out,
                                                                double* __restrict__ proj_out) {
   const NodeDesc nd = nodes[blockIdx.x];
@@ -393,6 +389,7 @@ __global__ void __launch_bounds__(kThreads, 3) skeletonize_kernel(const NodeDesc
     rank_out[blockIdx.x] = rank;
     achieved_out[blockIdx.x] =
         (rank < size) ? __ddiv_rn(fabs(A[int64_t(rank) * ld + rank]), fmax(lead, 1e-300)) : 0.0;
+    if (lead_out) lead_out[blockIdx.x] = lead;
   }
   __syncthreads();
   // proj = Zero(rank, cols); proj(l, perm[l]) = 1; proj(:, perm[j]) = R11^{-1} R12(:, j - rank)
@@ -430,6 +427,89 @@ int skel_fail(int code, const char* what, cudaError_t e = cudaSuccess) {
 }
 }  // namespace
 
+namespace gofmm_skel {
+
+double algorithmic_bytes(const std::vector<NodeDesc>& nd, double* flops_out) {
+  // step k streams the (rows-k) x (cols-k) trailing block three times (Householder dot, update
+  // read, update write), plus the transpose in and proj out
+  double bytes = 0.0, flops = 0.0;
+  for (const NodeDesc& q : nd) {
+    const int sz = std::min(q.rows, q.cols);
+    for (int k = 0; k < sz; ++k) {
+      const double tb = double(q.rows - k) * double(q.cols - k - 1);
+      bytes += 24.0 * tb;
+      flops += 4.0 * tb;
+    }
+    bytes += 16.0 * double(q.rows) * q.cols;
+  }
+  if (flops_out) *flops_out = flops;
+  return bytes;
+}
+
+int skel_device(std::vector<NodeDesc>& nd, const double* d_in, int32_t s, double tau, int32_t* rank_out,
+                double* achieved_out, double* lead_out, int32_t* perm_out, double* proj_out, float* kernel_ms,
+                std::string* err) {
+  auto fail = [&](int code, const char* what, cudaError_t e) {
+    if (err) *err = std::string(what) + (e != cudaSuccess ? std::string(": ") + cudaGetErrorString(e) : "");
+    return code;
+  };
+  const int nnodes = int(nd.size());
+  if (nnodes == 0) return GOFMM_OK;
+  int64_t ws = 0, pe = 0, pj = 0;
+  int max_rows = 0, max_cols = 0;
+  for (NodeDesc& q : nd) {
+    q.ws_off = ws;
+    q.perm_off = pe;
+    q.proj_off = pj;
+    ws += int64_t(q.rows) * ((q.cols + 1) & ~1);  // row-major, even ld (kernel)
+    pe += q.cols;
+    pj += int64_t(std::min({s, q.rows, q.cols})) * q.cols;
+    max_rows = std::max(max_rows, int(q.rows));
+    max_cols = std::max(max_cols, int(q.cols));
+  }
+  const size_t smem = size_t(2 * max_cols + 2 * max_rows) * sizeof(double) + size_t(max_cols) * sizeof(int);
+  if (smem > 200 * 1024) return fail(GOFMM_ERR_INVALID, "skeletonize_batch: block too large for one CTA", cudaSuccess);
+  DBuf d_nd, d_ws, d_rank, d_ach, d_lead, d_perm, d_proj;
+  cudaError_t e;
+  auto al = [&](DBuf& b, size_t bytes) { return cudaMalloc(&b.p, std::max<size_t>(bytes, 8)); };
+  if ((e = al(d_nd, nd.size() * sizeof(NodeDesc))) != cudaSuccess || (e = al(d_ws, ws * 8)) != cudaSuccess ||
+      (e = al(d_rank, nnodes * 4)) != cudaSuccess || (e = al(d_ach, nnodes * 8)) != cudaSuccess ||
+      (e = al(d_lead, nnodes * 8)) != cudaSuccess || (e = al(d_perm, pe * 4)) != cudaSuccess ||
+      (e = al(d_proj, pj * 8)) != cudaSuccess)
+    return fail(GOFMM_ERR_CUDA, "skeletonize_batch: device allocation", e);
+  if ((e = cudaMemcpy(d_nd.p, nd.data(), nd.size() * sizeof(NodeDesc), cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(skeletonize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) !=
+          cudaSuccess)
+    return fail(GOFMM_ERR_CUDA, "skeletonize_batch: upload", e);
+  cudaEvent_t ev[2];
+  cudaEventCreate(&ev[0]);
+  cudaEventCreate(&ev[1]);
+  cudaEventRecord(ev[0]);
+  skeletonize_kernel<<<unsigned(nnodes), kThreads, smem>>>(
+      static_cast<NodeDesc*>(d_nd.p), d_in, static_cast<double*>(d_ws.p), s, tau, static_cast<int32_t*>(d_rank.p),
+      static_cast<double*>(d_ach.p), static_cast<double*>(d_lead.p), static_cast<int32_t*>(d_perm.p),
+      static_cast<double*>(d_proj.p));
+  cudaEventRecord(ev[1]);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaEventSynchronize(ev[1]);
+  float ms = 0.f;
+  if (e == cudaSuccess) cudaEventElapsedTime(&ms, ev[0], ev[1]);
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  if (e != cudaSuccess) return fail(GOFMM_ERR_CUDA, "skeletonize_batch: kernel", e);
+  if (kernel_ms) *kernel_ms = ms;
+  // proj: per node maxrank x cols slot, of which rank x cols (ld = rank) is written
+  if ((e = cudaMemcpy(rank_out, d_rank.p, size_t(nnodes) * 4, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+      (e = cudaMemcpy(achieved_out, d_ach.p, size_t(nnodes) * 8, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+      (lead_out && (e = cudaMemcpy(lead_out, d_lead.p, size_t(nnodes) * 8, cudaMemcpyDeviceToHost)) != cudaSuccess) ||
+      (e = cudaMemcpy(perm_out, d_perm.p, size_t(pe) * 4, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+      (e = cudaMemcpy(proj_out, d_proj.p, size_t(pj) * 8, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return fail(GOFMM_ERR_CUDA, "skeletonize_batch: download", e);
+  return GOFMM_OK;
+}
+
+}  // namespace gofmm_skel
+
 extern "C" {
 
 const char* gofmm_skeletonize_last_error(void) { return g_skel_err; }
@@ -449,80 +529,27 @@ int gofmm_skeletonize_batch(int32_t nnodes, const int32_t* rows, const int32_t* 
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return skel_fail(GOFMM_ERR_CUDA, "cudaSetDevice", e);
   std::vector<NodeDesc> nd(static_cast<size_t>(nnodes));
-  int64_t in_elems = 0, ws = 0, pe = 0, pj = 0;
-  int max_rows = 0, max_cols = 0;
+  int64_t in_elems = 0;
   for (int32_t t = 0; t < nnodes; ++t) {
     if (rows[t] < 1 || cols[t] < 1 || block_off[t] < 0)
       return skel_fail(GOFMM_ERR_INVALID, "skeletonize_batch: every node needs rows, cols >= 1");
-    nd[t] = {block_off[t], ws, pe, pj, rows[t], cols[t]};
+    nd[t] = {block_off[t], 0, 0, 0, rows[t], cols[t]};
     in_elems = std::max(in_elems, block_off[t] + int64_t(rows[t]) * cols[t]);
-    ws += int64_t(rows[t]) * ((cols[t] + 1) & ~1);  // row-major, even ld (kernel)
-    pe += cols[t];
-    pj += int64_t(std::min({s, rows[t], cols[t]})) * cols[t];
-    max_rows = std::max(max_rows, int(rows[t]));
-    max_cols = std::max(max_cols, int(cols[t]));
   }
-  const size_t smem = size_t(2 * max_cols + 2 * max_rows) * sizeof(double) + size_t(max_cols) * sizeof(int);
-  if (smem > 200 * 1024) return skel_fail(GOFMM_ERR_INVALID, "skeletonize_batch: block too large for one CTA");
-  DBuf d_nd, d_in, d_ws, d_rank, d_ach, d_perm, d_proj;
-  auto al = [&](DBuf& b, size_t bytes) { return cudaMalloc(&b.p, std::max<size_t>(bytes, 8)); };
-  if ((e = al(d_nd, nd.size() * sizeof(NodeDesc))) != cudaSuccess || (e = al(d_in, in_elems * 8)) != cudaSuccess ||
-      (e = al(d_ws, ws * 8)) != cudaSuccess || (e = al(d_rank, nnodes * 4)) != cudaSuccess ||
-      (e = al(d_ach, nnodes * 8)) != cudaSuccess || (e = al(d_perm, pe * 4)) != cudaSuccess ||
-      (e = al(d_proj, pj * 8)) != cudaSuccess)
-    return skel_fail(GOFMM_ERR_CUDA, "skeletonize_batch: device allocation", e);
-  cudaEvent_t ev[2];
-  cudaEventCreate(&ev[0]);
-  cudaEventCreate(&ev[1]);
   auto t0 = std::chrono::steady_clock::now();
-  if ((e = cudaMemcpy(d_nd.p, nd.data(), nd.size() * sizeof(NodeDesc), cudaMemcpyHostToDevice)) != cudaSuccess ||
-      (e = cudaMemcpy(d_in.p, blocks, size_t(in_elems) * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
-      (e = cudaFuncSetAttribute(skeletonize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) !=
-          cudaSuccess) {
-    cudaEventDestroy(ev[0]);
-    cudaEventDestroy(ev[1]);
+  DBuf d_in;
+  if ((e = cudaMalloc(&d_in.p, std::max<size_t>(size_t(in_elems) * 8, 8))) != cudaSuccess ||
+      (e = cudaMemcpy(d_in.p, blocks, size_t(in_elems) * 8, cudaMemcpyHostToDevice)) != cudaSuccess)
     return skel_fail(GOFMM_ERR_CUDA, "skeletonize_batch: upload", e);
-  }
-  cudaEventRecord(ev[0]);
-  skeletonize_kernel<<<unsigned(nnodes), kThreads, smem>>>(
-      static_cast<NodeDesc*>(d_nd.p), static_cast<double*>(d_in.p), static_cast<double*>(d_ws.p), s, tau,
-      static_cast<int32_t*>(d_rank.p), static_cast<double*>(d_ach.p), static_cast<int32_t*>(d_perm.p),
-      static_cast<double*>(d_proj.p));
-  cudaEventRecord(ev[1]);
-  e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaEventSynchronize(ev[1]);
-  if (e != cudaSuccess) {
-    cudaEventDestroy(ev[0]);
-    cudaEventDestroy(ev[1]);
-    return skel_fail(GOFMM_ERR_CUDA, "skeletonize_batch: kernel", e);
-  }
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, ev[0], ev[1]);
-  cudaEventDestroy(ev[0]);
-  cudaEventDestroy(ev[1]);
-  // proj: per node maxrank x cols slot, of which rank x cols (ld = rank) is written
-  if ((e = cudaMemcpy(rank_out, d_rank.p, size_t(nnodes) * 4, cudaMemcpyDeviceToHost)) != cudaSuccess ||
-      (e = cudaMemcpy(achieved_out, d_ach.p, size_t(nnodes) * 8, cudaMemcpyDeviceToHost)) != cudaSuccess ||
-      (e = cudaMemcpy(perm_out, d_perm.p, size_t(pe) * 4, cudaMemcpyDeviceToHost)) != cudaSuccess ||
-      (e = cudaMemcpy(proj_out, d_proj.p, size_t(pj) * 8, cudaMemcpyDeviceToHost)) != cudaSuccess)
-    return skel_fail(GOFMM_ERR_CUDA, "skeletonize_batch: download", e);
+  std::string err;
+  const int rc = skel_device(nd, static_cast<const double*>(d_in.p), s, tau, rank_out, achieved_out, nullptr, perm_out,
+                             proj_out, &ms, &err);
+  if (rc != GOFMM_OK) return skel_fail(rc, err.c_str());
   if (stats) {
     stats->kernel_ms = ms;
     stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    // algorithmic bytes: step k streams the (rows-k) x (cols-k) trailing block three times
-    // (Householder dot, update read, update write), plus the transpose in and proj out
-    double bytes = 0.0, flops = 0.0;
-    for (const NodeDesc& q : nd) {
-      const int sz = std::min(q.rows, q.cols);
-      for (int k = 0; k < sz; ++k) {
-        const double tb = double(q.rows - k) * double(q.cols - k - 1);
-        bytes += 24.0 * tb;
-        flops += 4.0 * tb;
-      }
-      bytes += 16.0 * double(q.rows) * q.cols;
-    }
-    stats->bytes = bytes;
-    stats->flops = flops;
+    stats->bytes = algorithmic_bytes(nd, &stats->flops);
   }
   return GOFMM_OK;
 }
