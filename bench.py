@@ -2,9 +2,12 @@
 """bench.py — GOFMM evaluation phase u = K~ W on B200 (BASELINE.json metric, config 3 by default).
 
 One "step" = one evaluation of the c3 workload (N = 2^20 COVTYPE-shaped d=8 points, Gaussian h=1,
-m = s = 512, budget 0.03, r = 512 RHS, FP64) over a synthetic compressed tree of that shape
-(paper_1707_00164_b200/synth.py; the reference compress needs hours at 1M and has no HMatrix file
-format). Inputs (W, 4.3 GB) exceed L2 (126 MB), so no extra flush is needed between steps.
+m = s = 512, budget 0.03, r = 512 RHS, FP64) over the compressed tree the product compress
+(gofmm_compress: the reference compress algorithm, GPU entries) builds from that cloud before the
+timed region (~45 s at 1M; --tree synth: synth.py's saturated-rank tree). Inputs (W, 4.3 GB) exceed
+L2 (126 MB), so no extra flush is needed between steps. The CPU legs (reference arm, cpu_baseline,
+same-config GPU leg) share one bounded sample: the reference compress() of the config's cloud at
+N = 2^16.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
 
@@ -174,14 +177,48 @@ def host_info() -> dict:
     return info
 
 
-def cpu_sample_tree(cfg: dict, n_sample: int, seed: int):
-    """A bounded sample of the workload: a c3-shaped tree (same d, m, s, budget, kernel) on
-    n_sample points — the SAME tree for the reference arm, the cpu_baseline leg and the GPU's
-    same-config leg."""
+def config_cloud(cfg: dict, n: int, seed: int) -> np.ndarray:
+    """The config's synthetic point cloud (d x n): uniform [0,1]^d (c1), standard normal (c2, c4,
+    c5), COVTYPE-shaped Gaussian mixture (c3) — synth.py."""
     from paper_1707_00164_b200 import synth
 
-    tree, _ = synth.make_config_tree(cfg["name"], seed=seed, n=n_sample, budget=cfg["budget"])
-    return tree
+    fn = {"uniform": synth.uniform_cloud, "gaussian": synth.gaussian_cloud, "covtype": synth.covtype_like}[cfg["cloud"]]
+    return fn(n, cfg["d"], seed)
+
+
+def workload_tree(cfg: dict, n: int, seed: int, source: str):
+    """The timed tree. "compress": the product compress (gofmm_compress: the reference's compress
+    algorithm with ANN passes, sampled blocks and CPQR on the GPU) of the config's cloud with the
+    config's kernel / m / s / budget and the reference RunConfig defaults otherwise (tau 1e-5,
+    kappa 32, kernel distance, 10 ANN iterations); "synth": synth.py's saturated-rank tree."""
+    from paper_1707_00164_b200 import compress, synth
+
+    if source == "synth":
+        tree, _ = synth.make_config_tree(cfg["name"], seed=seed, n=n, budget=cfg["budget"])
+        return tree, {"tree": "synthetic saturated-rank tree (synth.py)"}
+    pc = config_cloud(cfg, n, seed)
+    res = compress(pc, cfg["kernel"], (cfg["h"], 0.0), m=cfg["m"], s=cfg["s"], budget=cfg["budget"], tau=1e-5,
+                   kappa=32, distance="kernel", seed=seed, threads=os.cpu_count() or 1, entries="device")
+    st = res.stats
+    info = {"tree": "product compress (gofmm_compress, GPU entries) of the config's cloud",
+            "compress": {"seconds": round(st["compress_seconds"], 2), "mean_rank": round(st["mean_skeleton"], 1),
+                         "max_rank": st["max_skeleton"], "entries_evaluated": st["entries_evaluated"],
+                         "ann_recall_last": round(st["ann_recall"][-1], 4) if st["ann_recall"] else None}}
+    return res.tree, info
+
+
+def cpu_sample_tree(cfg: dict, n_sample: int, seed: int):
+    """A bounded sample of the workload for the CPU legs: the REFERENCE compress() (oracle/_ref) of
+    the config's cloud at n_sample points (same d, kernel, m, s, budget, RunConfig defaults) — the
+    SAME HMatrix for the reference arm, the cpu_baseline leg and the GPU's same-config leg.
+    Returns (reference HMatrix, its flattened tree)."""
+    from oracle import refpy as R
+    from paper_1707_00164_b200 import CompressedTree
+
+    pc = config_cloud(cfg, n_sample, seed)
+    h = R.compress_kernel(cfg["kernel"], pc, cfg["h"], 0.0, m=cfg["m"], s=cfg["s"], tau=1e-5, kappa=32,
+                          budget=cfg["budget"], seed=seed, threads=os.cpu_count() or 1)
+    return h, CompressedTree.from_any(h.export(blocks=False))
 
 
 def sample_rhs(n: int, r: int) -> np.ndarray:
@@ -220,17 +257,14 @@ def reference_arm(args, world, rank):
     cfg["name"] = args.config
     r = args.r or cfg["r"]
     threads = os.cpu_count() or 1
-    tree = cpu_sample_tree(cfg, min(args.cpu_n, cfg["n"]), seed=args.seed)
-    from oracle import refpy as R
-
-    ref = R.import_flat(tree, threads=threads)
+    ref, tree = cpu_sample_tree(cfg, min(args.cpu_n, cfg["n"]), seed=args.seed)
     w = sample_rhs(tree.n, r)
     res = cpu_protocol(ref, w, threads, reps=max(args.steps, 3), warmup=max(args.warmup, 1))
     sec = res["task_dag"]["median_s"]
     val = res["flops"] / sec / 1e9
-    sample = (f"{args.config}-shaped tree at N={tree.n} (same d/m/s/budget/kernel, synth.py seed {args.seed}), "
-              f"r={r}; reference gfmm::evaluate, TaskDag x{threads} threads, median of {max(args.steps, 3)} "
-              f"Potentials.seconds after {max(args.warmup, 1)} warm-up")
+    sample = (f"{args.config} cloud at N={tree.n} compressed by the reference compress() (same d/kernel/m/s/"
+              f"budget, seed {args.seed}), r={r}; reference gfmm::evaluate, TaskDag x{threads} threads, median of "
+              f"{max(args.steps, 3)} Potentials.seconds after {max(args.warmup, 1)} warm-up")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sec, 3), "higher_is_better": True,
@@ -302,9 +336,9 @@ def ours_arm(args, world, rank, local):
     if args.n:
         cfg["n"] = args.n
     r = args.r or cfg["r"]
+    cfg["name"] = args.config
     t0 = time.perf_counter()
-    tree, cfg = synth.make_config_tree(args.config, seed=args.seed,
-                                       **{k: cfg[k] for k in ("n", "budget")})
+    tree, tree_info = workload_tree(cfg, cfg["n"], args.seed, args.tree)
     t_gen = time.perf_counter() - t0
     f32 = args.precision == "fp32"
     tdt = torch.float32 if f32 else torch.float64
@@ -376,6 +410,13 @@ def ours_arm(args, world, rank, local):
     except Exception:
         pass
 
+    # the BASELINE metric's "rel. error" on the timed tree itself: the reference's error_eps2
+    # (evaluate.hpp:330-373; r = 1, 100 sampled rows, the reference Rng draws) computed by the
+    # product — GPU evaluation + matrix-free exact rows on the GPU
+    eps2 = None
+    if not f32:
+        eps2 = ev.error_eps2(1, 100, args.seed)["eps2"]
+
     # end-to-end through the host API (pinned host W and u; H2D + D2H inside the timed region)
     e2e = None
     if not args.no_e2e:
@@ -408,20 +449,18 @@ def ours_arm(args, world, rank, local):
         try:
             from oracle import refpy as R
 
-            cfg_s = dict(cfg)
-            cfg_s["name"] = args.config
-            stree = cpu_sample_tree(cfg_s, min(args.cpu_n, tree.n), seed=args.seed)
+            ref, stree = cpu_sample_tree(cfg, min(args.cpu_n, tree.n), seed=args.seed)
             threads = os.cpu_count() or 1
             ws = sample_rhs(stree.n, r)
-            ref = R.import_flat(stree, threads=threads)
             res = cpu_protocol(ref, ws, threads, reps=3, warmup=1)
             del ref
             cpu_sec = res["task_dag"]["median_s"]
             cpu_val = res["flops"] / cpu_sec / 1e9
             cpu = {"value": round(cpu_val, 3), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
-                   "sample": f"{args.config}-shaped tree at N={stree.n} (same d/m/s/budget/kernel, synth.py seed "
-                             f"{args.seed}), r={r}; reference gfmm::evaluate, TaskDag x{threads} threads, median of 3 "
-                             f"Potentials.seconds after 1 warm-up (the reference arm's protocol)",
+                   "sample": f"{args.config} cloud at N={stree.n} compressed by the reference compress() (same "
+                             f"d/kernel/m/s/budget, seed {args.seed}), r={r}; reference gfmm::evaluate, TaskDag "
+                             f"x{threads} threads, median of 3 Potentials.seconds after 1 warm-up (the reference "
+                             f"arm's protocol)",
                    "level_by_level_gflops": round(res["flops"] / res["level_by_level"]["median_s"] / 1e9, 3),
                    "runs_s": res["task_dag"]["runs_s"], "host": host_info()}
             sc = same_config_leg(Evaluator, stree, ws, args.precision, local)
@@ -447,7 +486,7 @@ def ours_arm(args, world, rank, local):
                                f"s={cfg['s']} budget={cfg['budget']} r={r} per GPU", "n": tree.n, "d": cfg["d"],
                    "m": cfg["m"], "s": cfg["s"], "budget": cfg["budget"], "r_per_gpu": r,
                    "near_pairs": int(len(tree.near_a)), "far_pairs": int(len(tree.far_a)),
-                   "tree": "synthetic saturated-rank tree (synth.py)", "l2_flush": (f"L2 flushed between steps (256 MB write, outside the per-step events); W {tree.n * r * esz / 1e6:.1f} MB" if small else f"inputs larger than L2 (W {tree.n * r * esz / 1e9:.2f} GB)"),
+                   **tree_info, "l2_flush": (f"L2 flushed between steps (256 MB write, outside the per-step events); W {tree.n * r * esz / 1e6:.1f} MB" if small else f"inputs larger than L2 (W {tree.n * r * esz / 1e9:.2f} GB)"),
                    "parallelism": "single GPU", "precision": args.precision,
                    "arithmetic": "3xTF32 on tcgen05 (FP32 accumulate in TMEM)" if f32 else "FP64 DMMA"},
         "sec_per_eval": round(ms / 1e3, 6),
@@ -455,6 +494,7 @@ def ours_arm(args, world, rank, local):
         "flops_per_eval": int(flops),
         "rel_error": rel_err,
         "rel_error_tree": (same or {}).get("tree"),
+        "eps2_timed_tree": eps2,
         "phase_ms": {k: round(v[1], 3) for k, v in phases.items()} | {"permute": round(ph["ms_permute"], 3)},
         "roofline": {"bound": "tensor", "kernel": dom_name, "achieved": round(achieved, 3),
                      "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -490,9 +530,20 @@ def dist_arm(args, world, rank, local):
     if args.n:
         cfg["n"] = args.n
     r = args.r or cfg["r"]
+    cfg["name"] = args.config
     t0 = time.perf_counter()
-    tree, cfg = synth.make_config_tree(args.config, seed=args.seed, **{k: cfg[k] for k in ("n", "budget")})
+    tree, tree_info = workload_tree(cfg, cfg["n"], args.seed, args.tree)
     t_gen = time.perf_counter() - t0
+    if world > 1:  # every rank compressed the same cloud; the GPU compress is deterministic — check
+        import hashlib
+
+        hsh = hashlib.sha256()
+        for f in ("iperm", "rank", "skel_idx", "proj", "near_a", "near_b", "far_a", "far_b"):
+            hsh.update(np.ascontiguousarray(getattr(tree, f)).tobytes())
+        digests = [None] * world
+        dist.all_gather_object(digests, hsh.hexdigest())
+        if len(set(digests)) != 1:
+            raise RuntimeError(f"ranks built different trees: {digests}")
     t0 = time.perf_counter()
     f32 = args.precision == "fp32"
     tdt = torch.float32 if f32 else torch.float64
@@ -590,7 +641,7 @@ def dist_arm(args, world, rank, local):
         "vs_baseline": None, "dtype": "f32" if f32 else "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {KERNEL_NAMES.get(cfg['kernel'], 'kernel')} h={cfg['h']} N={tree.n} "
                                f"d={cfg['d']} m={cfg['m']} s={cfg['s']} budget={cfg['budget']} r={r} total",
-                   "n": tree.n, "r": r, "budget": cfg["budget"], "parallelism": f"subtree split x{world}",
+                   "n": tree.n, "r": r, "budget": cfg["budget"], "parallelism": f"subtree split x{world}", **tree_info,
                    "split_level": info["split_level"], "allgather_bytes_per_rank": int(slot * esz),
                    "exchange": "in-library ncclAllGather (gofmm_dist_evaluate), W replicated, what only",
                    "l2_flush": f"inputs larger than L2 (W {tree.n * r * esz / 1e9:.2f} GB)",
@@ -630,6 +681,8 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
     ap.add_argument("--budget", type=float, default=None)
+    ap.add_argument("--tree", default="compress", choices=["compress", "synth"],
+                    help="timed tree: the product compress of the config's cloud (default) or synth.py's")
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--r", type=int, default=None)
     ap.add_argument("--seed", type=int, default=0)
