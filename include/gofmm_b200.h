@@ -349,6 +349,31 @@ int gofmm_compressed_stats(const gofmm_compressed* c, gofmm_compress_stats* stat
 int gofmm_compressed_free(gofmm_compressed* c);
 const char* gofmm_compress_last_error(void);
 
+/* ---- error_eps2 (evaluate.hpp:330-373) ------------------------------------------------------
+ * ErrorReport (evaluate.hpp:319-326) of this handle's evaluation against exact rows of K: the
+ * reference's draws (gofmm_rng_eps2_draw_attempt, up to 3 W draws), u = K~ W on the device, the exact
+ * rows K(rows, :) W generated matrix-free on the device (kernel sources only). rows_out (optional)
+ * receives the min(sample_rows, n) sampled original indices. A degenerate draw three times in a
+ * row -> GOFMM_ERR_NUMERIC (the reference's numeric_error). */
+typedef struct gofmm_eps2_report {
+  double eps2;
+  double per_entry[10]; /* relative row errors of the first 10 sampled rows */
+  int32_t num_per_entry;
+  double mean_sample;   /* average relative row error over the sample */
+  int64_t eval_flops;
+  double eval_seconds;
+} gofmm_eps2_report;
+int gofmm_error_eps2(gofmm_handle* h, int32_t r, int32_t sample_rows, uint64_t seed, gofmm_eps2_report* rep,
+                     int32_t* rows_out);
+
+/* ---- point sources of the CLI (tools/gfmm_cli.cpp:55-92) ---------------------------------------
+ * PointCloud::random_gaussian(n, d, seed) (oracle.hpp:18-25) into out (d x n column-major), and
+ * default_laplace_floor(points, seed) (oracle.hpp:274-288). */
+int gofmm_points_gaussian(int32_t n, int32_t d, uint64_t seed, double* out);
+int gofmm_default_laplace_floor(int32_t d, int32_t n, const double* coords, uint64_t seed, double* out);
+/* Rng(seed, stream).gauss() (common.hpp:52-77) column-major into w (n x r, leading dimension ldw). */
+int gofmm_rng_gauss_stream(uint64_t seed, uint64_t stream, int32_t n, int32_t r, double* w, int64_t ldw);
+
 /* Bytes of device memory held by the handle (tree + workspace). */
 int64_t gofmm_device_bytes(const gofmm_handle* h);
 

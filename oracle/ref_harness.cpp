@@ -176,11 +176,11 @@ static std::unique_ptr<EntryOracle> make_kernel(int32_t kernel, const PointCloud
 }
 
 // Laplace default floor (oracle.hpp:276-288) so callers can pass the resolved value to the GPU.
-double gfmm_ref_default_laplace_floor(const double* coords, int32_t d, int32_t n) {
+double gfmm_ref_default_laplace_floor(const double* coords, int32_t d, int32_t n, uint64_t seed) {
   PointCloud pc;
   pc.coords.resize(d, n);
   std::memcpy(pc.coords.data(), coords, sizeof(double) * size_t(d) * size_t(n));
-  return default_laplace_floor(pc);
+  return default_laplace_floor(pc, seed);
 }
 
 int gfmm_ref_compress_kernel(int32_t kernel, const double* coords, int32_t d, int32_t n, double p0,

@@ -119,7 +119,7 @@ def lib():
         L.gfmm_ref_rng_gauss.argtypes = [C.c_int64, C.c_int32, C.c_uint64, C.c_uint64, _P]
         L.gfmm_ref_splitmix64.argtypes = [C.c_uint64]
         L.gfmm_ref_splitmix64.restype = C.c_uint64
-        L.gfmm_ref_default_laplace_floor.argtypes = [_P, C.c_int32, C.c_int32]
+        L.gfmm_ref_default_laplace_floor.argtypes = [_P, C.c_int32, C.c_int32, C.c_uint64]
         L.gfmm_ref_default_laplace_floor.restype = C.c_double
         L.gfmm_ref_dense.argtypes = [_P, _P]
         L.gfmm_ref_exact_rows.argtypes = [_P, _P, C.c_int32, _P, C.c_int32, _P]
@@ -180,9 +180,9 @@ def splitmix64(x: int) -> int:
     return int(lib().gfmm_ref_splitmix64(x))
 
 
-def default_laplace_floor(coords: np.ndarray) -> float:
+def default_laplace_floor(coords: np.ndarray, seed: int = 0) -> float:
     c = np.asfortranarray(coords, dtype=np.float64)
-    return float(lib().gfmm_ref_default_laplace_floor(_ptr(c), c.shape[0], c.shape[1]))
+    return float(lib().gfmm_ref_default_laplace_floor(_ptr(c), c.shape[0], c.shape[1], seed))
 
 
 def eps2_draw(n: int, r: int, sample_rows: int, seed: int):

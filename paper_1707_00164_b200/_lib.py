@@ -13,6 +13,7 @@ import sys
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_DIR = os.path.dirname(PKG_DIR)
 LIB_PATH = os.path.join(PKG_DIR, "_lib", "libgofmm_b200.so")
+CLI_PATH = os.path.join(PKG_DIR, "_lib", "gofmm_b200_cli")
 CSRC = os.path.join(PKG_DIR, "csrc")
 INCLUDE = os.path.join(REPO_DIR, "include")
 
@@ -43,11 +44,11 @@ UNITS = ("gofmm_capi.cu", "gofmm_f32.cu", "gofmm_skel.cu", "gofmm_ann.cu", "gofm
 
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile the CUDA extension in-tree with nvcc for sm_100a (cross-compiles without a GPU)."""
-    srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cu", ".cuh", ".h"))]
+    srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cu", ".cuh", ".h", ".cpp"))]
     srcs.append(os.path.join(INCLUDE, "gofmm_b200.h"))
-    if not force and os.path.exists(LIB_PATH):
+    if not force and os.path.exists(LIB_PATH) and os.path.exists(CLI_PATH):
         newest = max(os.path.getmtime(s) for s in srcs)
-        if os.path.getmtime(LIB_PATH) >= newest:
+        if min(os.path.getmtime(LIB_PATH), os.path.getmtime(CLI_PATH)) >= newest:
             return LIB_PATH
     out_dir = os.path.dirname(LIB_PATH)
     os.makedirs(out_dir, exist_ok=True)
@@ -68,6 +69,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     subprocess.run(cmd, check=True)
     for obj in objs:
         os.remove(obj)
+    # the command-line driver (gfmm_cli compress / bench over the C-ABI), next to the library
+    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-std=c++17", "-o", CLI_PATH, os.path.join(CSRC, "gofmm_cli.cpp"), "-L", out_dir,
+           "-lgofmm_b200", "-Xlinker", "-rpath,$ORIGIN"]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
     return LIB_PATH
 
 
@@ -138,7 +145,13 @@ EXPORTS = ("gofmm_create", "gofmm_evaluate", "gofmm_evaluate_device", "gofmm_unp
            "gofmm_ann_last_error", "gofmm_rng_eps2_draw_attempt", "gofmm_nccl_unique_id", "gofmm_dist_init_comm",
            "gofmm_dist_attach_comm", "gofmm_dist_evaluate", "gofmm_dist_evaluate_f32", "gofmm_compress_default_config",
            "gofmm_compress", "gofmm_compressed_desc", "gofmm_compressed_stats", "gofmm_compressed_free",
-           "gofmm_compress_last_error")
+           "gofmm_compress_last_error", "gofmm_error_eps2", "gofmm_points_gaussian",
+           "gofmm_default_laplace_floor", "gofmm_rng_gauss_stream")
+
+
+class Eps2Report(C.Structure):
+    _fields_ = [("eps2", C.c_double), ("per_entry", C.c_double * 10), ("num_per_entry", C.c_int32),
+                ("mean_sample", C.c_double), ("eval_flops", C.c_int64), ("eval_seconds", C.c_double)]
 
 
 class SkelStats(C.Structure):
@@ -182,6 +195,10 @@ def lib():
         L.gofmm_dist_attach_comm.argtypes = [P, P]
         L.gofmm_dist_evaluate.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, P, C.c_int32, P]
         L.gofmm_dist_evaluate_f32.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, P, C.c_int32, P]
+        L.gofmm_error_eps2.argtypes = [P, C.c_int32, C.c_int32, C.c_uint64, C.POINTER(Eps2Report), P]
+        L.gofmm_points_gaussian.argtypes = [C.c_int32, C.c_int32, C.c_uint64, P]
+        L.gofmm_default_laplace_floor.argtypes = [C.c_int32, C.c_int32, P, C.c_uint64, P]
+        L.gofmm_rng_gauss_stream.argtypes = [C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, P, C.c_int64]
         L.gofmm_device_bytes.argtypes = [P]
         L.gofmm_device_bytes.restype = C.c_int64
         L.gofmm_launches_per_eval.argtypes = [P]

@@ -2758,6 +2758,95 @@ int gofmm_rng_eps2_draw_attempt(uint64_t seed, int32_t n, int32_t r, int32_t sam
   });
 }
 
+// error_eps2 (evaluate.hpp:330-373) on the GPU: the reference's draws (rows, then W column-major
+// from Rng(seed, 0xe952), up to three W draws while the sampled rows of K w vanish), u = K~ W by
+// this handle's evaluation, the exact rows K(rows, :) W matrix-free on the device, and the report
+// fields of ErrorReport. Host W / u live only for the call.
+int gofmm_error_eps2(gofmm_handle* H, int32_t r, int32_t sample_rows, uint64_t seed, gofmm_eps2_report* rep,
+                     int32_t* rows_out) {
+  return guarded([&] {
+    if (!H || !rep) throw Error(GOFMM_ERR_INVALID, "error_eps2: null argument");
+    if (sample_rows < 1) throw Error(GOFMM_ERR_INVALID, "sample_rows must be >= 1");
+    if (r < 1) throw Error(GOFMM_ERR_INVALID, "r must be >= 1");
+    if (H->nranks > 1) throw Error(GOFMM_ERR_INVALID, "error_eps2: single-GPU handles only");
+    const int n = H->n, k = std::min(sample_rows, n);
+    std::memset(rep, 0, sizeof(*rep));
+    std::vector<int32_t> rows(k);
+    std::vector<double> w(size_t(n) * r), u(size_t(n) * r), ex(size_t(k) * r);
+    std::vector<float> wf, uf;
+    const bool f32 = H->precision == GOFMM_PRECISION_F32;
+    if (f32) {
+      wf.resize(w.size());
+      uf.resize(u.size());
+    }
+    double* d_w = nullptr;
+    double* d_ex = nullptr;
+    GOFMM_CUDA(cudaSetDevice(H->device));
+    GOFMM_CUDA(cudaMalloc(&d_w, w.size() * sizeof(double)));
+    GOFMM_CUDA(cudaMalloc(&d_ex, ex.size() * sizeof(double)));
+    struct Free {
+      double *a, *b;
+      ~Free() {
+        cudaFree(a);
+        cudaFree(b);
+      }
+    } fr{d_w, d_ex};
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      int rc = gofmm_rng_eps2_draw_attempt(seed, n, r, sample_rows, attempt, rows.data(), w.data(), n);
+      if (rc != GOFMM_OK) throw Error(rc, g_last_error);
+      gofmm_eval_stats st{};
+      if (f32) {
+        for (size_t q = 0; q < w.size(); ++q) wf[q] = float(w[q]);
+        rc = gofmm_evaluate_f32(H, wf.data(), n, r, uf.data(), n, &st);
+        for (size_t q = 0; q < u.size(); ++q) u[q] = double(uf[q]);
+      } else {
+        rc = gofmm_evaluate(H, w.data(), n, r, u.data(), n, &st);
+      }
+      if (rc != GOFMM_OK) throw Error(rc, g_last_error);
+      rep->eval_flops = st.flops;
+      rep->eval_seconds = st.seconds;
+      GOFMM_CUDA(cudaMemcpy(d_w, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice));
+      rc = gofmm_exact_rows(H, rows.data(), k, d_w, n, r, d_ex, k, nullptr);
+      if (rc != GOFMM_OK) throw Error(rc, g_last_error);
+      GOFMM_CUDA(cudaStreamSynchronize(H->stream));
+      GOFMM_CUDA(cudaMemcpy(ex.data(), d_ex, ex.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      // unpermute (evaluate.hpp:21-25): original row i sits at permuted position perm[i]
+      std::vector<int64_t> pos(k);
+      for (int t = 0; t < k; ++t) pos[t] = -1;
+      {
+        std::vector<int32_t> want(n, -1);
+        for (int t = 0; t < k; ++t) want[rows[t]] = t;
+        for (int t = 0; t < n; ++t)
+          if (want[H->iperm[t]] >= 0) pos[want[H->iperm[t]]] = t;
+      }
+      double num = 0.0, den = 0.0, sum_rel = 0.0;
+      std::vector<double> rel(k);
+      for (int t = 0; t < k; ++t) {
+        const int64_t pr = pos[t];
+        double dn = 0.0, de = 0.0;
+        for (int c = 0; c < r; ++c) {
+          const double e = ex[t + size_t(c) * k];
+          const double d = u[pr + size_t(c) * n] - e;
+          dn += d * d;
+          de += e * e;
+        }
+        num += dn;
+        den += de;
+        rel[t] = de > 0 ? std::sqrt(dn) / std::sqrt(de) : 0.0;
+      }
+      if (den == 0.0) continue;  // degenerate right-hand side; resample (evaluate.hpp:360)
+      rep->eps2 = std::sqrt(num / den);
+      rep->num_per_entry = std::min(k, 10);
+      for (int t = 0; t < rep->num_per_entry; ++t) rep->per_entry[t] = rel[t];
+      for (int t = 0; t < k; ++t) sum_rel += rel[t];
+      rep->mean_sample = sum_rel / double(k);
+      if (rows_out) std::copy(rows.begin(), rows.end(), rows_out);
+      return;
+    }
+    throw Error(GOFMM_ERR_NUMERIC, "error_eps2: sampled rows of Kw vanished repeatedly");
+  });
+}
+
 int gofmm_unpermute_device(gofmm_handle* H, const double* d_up, int64_t ldp, int32_t r, double* d_u, int64_t ldu,
                            void* stream) {
   return guarded([&] {

@@ -1222,3 +1222,64 @@ int gofmm_compressed_free(gofmm_compressed* R) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- point sources (CLI inputs)
+extern "C" {
+
+// PointCloud::random_gaussian (oracle.hpp:18-25): Rng(seed, 0x9f), point j outer, dimension i inner.
+int gofmm_points_gaussian(int32_t n, int32_t d, uint64_t seed, double* out) {
+  if (n < 1 || d < 1 || !out) {
+    gofmm::cmp::g_err = "points: need n >= 1, d >= 1 and an output buffer";
+    return GOFMM_ERR_INVALID;
+  }
+  gofmm::RefRng rng(seed, 0x9f);
+  for (int64_t j = 0; j < n; ++j)
+    for (int i = 0; i < d; ++i) out[j * d + i] = rng.gauss();
+  return GOFMM_OK;
+}
+
+// Rng(seed, stream).gauss() column-major into w (n x r, ld ldw): the bench RHS of the CLI,
+// Rng(cfg.seed, 0xbe7c) (gfmm_cli.cpp:195-198), and the tests' Rng(seed, 0) RHS.
+int gofmm_rng_gauss_stream(uint64_t seed, uint64_t stream, int32_t n, int32_t r, double* w, int64_t ldw) {
+  if (n < 1 || r < 1 || !w || ldw < n) {
+    gofmm::cmp::g_err = "rng: bad arguments";
+    return GOFMM_ERR_INVALID;
+  }
+  gofmm::RefRng rng(seed, stream);
+  for (int64_t c = 0; c < r; ++c)
+    for (int64_t i = 0; i < n; ++i) w[i + c * ldw] = rng.gauss();
+  return GOFMM_OK;
+}
+
+// default_laplace_floor (oracle.hpp:274-288): 1e-3 x the median pairwise distance of a 100-point
+// sample drawn from Rng(seed, 0x1ap1) (the hex-float literal is 52.0 -> stream 52); distances as the
+// reference computes them ((xa - xb).norm(): Eigen's packet reduction of the squares, then sqrt).
+int gofmm_default_laplace_floor(int32_t d, int32_t n, const double* coords, uint64_t seed, double* out) {
+  using gofmm::cmp::redux_packet;
+  if (n < 1 || d < 1 || !coords || !out) {
+    gofmm::cmp::g_err = "laplace floor: bad arguments";
+    return GOFMM_ERR_INVALID;
+  }
+  gofmm::RefRng rng(seed, 52);
+  const std::vector<int> sample = rng.sample_without_replacement(n, std::min(n, 100));
+  std::vector<double> dists;
+  for (size_t a = 0; a < sample.size(); ++a)
+    for (size_t b = a + 1; b < sample.size(); ++b) {
+      const double* xa = coords + int64_t(sample[a]) * d;
+      const double* xb = coords + int64_t(sample[b]) * d;
+      dists.push_back(std::sqrt(redux_packet(d, [&](int64_t q) {
+        const double e = xa[q] - xb[q];
+        return e * e;
+      })));
+    }
+  if (dists.empty()) {
+    *out = 1e-3;
+    return GOFMM_OK;
+  }
+  auto mid = dists.begin() + dists.size() / 2;
+  std::nth_element(dists.begin(), mid, dists.end());
+  *out = 1e-3 * *mid;
+  return GOFMM_OK;
+}
+
+}  // extern "C"

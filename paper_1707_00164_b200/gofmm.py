@@ -378,27 +378,19 @@ class Evaluator:
         return out.cpu().numpy()
 
     def error_eps2(self, r: int, sample_rows: int, seed: int) -> dict:
-        """Sampled relative error ||(K~w - Kw)_S||_F / ||(Kw)_S||_F with the reference's draws."""
+        """error_eps2 (evaluate.hpp:330-373) through gofmm_error_eps2: the reference's draws (rows,
+        then up to 3 W draws from Rng(seed, 0xe952)), this handle's evaluation and the exact rows of
+        K W generated on the device. Same report fields as ErrorReport (evaluate.hpp:319-326)."""
         if sample_rows < 1:
             raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "sample_rows must be >= 1")
         if r < 1:
             raise L.InvalidArgument(L.GOFMM_ERR_INVALID, "r must be >= 1")
-        # the reference redraws W from the same Rng stream up to 3 times while the sampled rows
-        # of K w vanish (evaluate.hpp:343-372); attempt a's W continues that stream
-        for attempt in range(3):
-            rows, w = rng_eps2_draw(seed, self.n, r, sample_rows, attempt)
-            pot = self.evaluate(w)
-            u = self.unpermute(pot.u)[rows]
-            exact = self.exact_rows(rows, w)
-            dn = np.linalg.norm(u - exact, axis=1)
-            de = np.linalg.norm(exact, axis=1)
-            num, den = float((dn ** 2).sum()), float((de ** 2).sum())
-            if den == 0.0:
-                continue
-            rel = np.where(de > 0, dn / np.where(de > 0, de, 1.0), 0.0)
-            return dict(eps2=float(np.sqrt(num / den)), per_entry=rel[:10].tolist(), mean_sample=float(rel.mean()),
-                        sample_rows=rows.tolist(), eval_flops=pot.flops, eval_seconds=pot.seconds)
-        raise L.GofmmError(L.GOFMM_ERR_NUMERIC, "error_eps2: sampled rows of Kw vanished repeatedly")
+        rep = L.Eps2Report()
+        rows = np.empty(min(sample_rows, self.n), dtype=np.int32)
+        L.check(L.lib().gofmm_error_eps2(self._h, int(r), int(sample_rows), int(seed), C.byref(rep), _p(rows)))
+        return dict(eps2=rep.eps2, per_entry=[rep.per_entry[i] for i in range(rep.num_per_entry)],
+                    mean_sample=rep.mean_sample, sample_rows=rows.tolist(), eval_flops=rep.eval_flops,
+                    eval_seconds=rep.eval_seconds)
 
     def unpermute(self, u_perm: np.ndarray) -> np.ndarray:
         """out.row(iperm[t]) = u_perm.row(t) (evaluate.hpp:21-25)."""
