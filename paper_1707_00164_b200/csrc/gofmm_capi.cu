@@ -499,6 +499,7 @@ struct gofmm_handle {
   cudaGraphExec_t gexec = nullptr;
   std::tuple<const void*, int64_t, const void*, int64_t, int32_t, int32_t, int32_t> gkey{};
   bool graphs = true;  // GOFMM_NO_GRAPH=1 disables replay
+  bool pdl = true;     // programmatic dependent launch between level launches (GOFMM_NO_PDL=1 disables)
   cudaEvent_t pev[2][4] = {};
   cudaEvent_t tev[2][4] = {};
   cudaEvent_t dpev[8][2] = {};  // per-part D2H timing of a split output launch (<= kOutParts)
@@ -782,6 +783,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     H->precision = o->precision;
   }
   if (const char* e = std::getenv("GOFMM_NO_GRAPH")) H->graphs = !(e[0] == '1');
+  if (const char* e = std::getenv("GOFMM_NO_PDL")) H->pdl = !(e[0] == '1');
   auto cp = [&](std::vector<int32_t>& v, const int32_t* p, int64_t k) { v.assign(p, p + k); };
   cp(H->parent, d->parent, nn);
   cp(H->left, d->left, nn);
@@ -1517,6 +1519,27 @@ struct LaunchCfg {
   const BMaps* maps;
   int bm_class;  // tile list: kBM[bm_class] rows per tile
 };
+// Programmatic dependent launch: the level launches of one evaluation form a chain of dependent
+// kernels; with the PDL attribute the next launch's CTAs are scheduled onto idle SMs as soon as
+// every CTA of the running launch has started (griddepcontrol.launch_dependents in its prologue),
+// run their own prologue, and block in griddepcontrol.wait until the running launch has completed
+// and its writes are visible — the launch gap between dependent levels disappears. Every kernel
+// launched this way calls griddepcontrol.wait before touching data an earlier launch writes.
+template <class... P, class... A>
+void launch_k(bool pdl, void (*fn)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  GOFMM_CUDA(cudaLaunchKernelEx(&cfg, fn, std::forward<A>(args)...));
+}
+
 // The widest tile that fits r is the most efficient per flop (generated entries and B tiles are
 // amortised over more columns), but a launch with few or very unequal term chains is bounded by
 // its longest chain, which a narrower N tile shortens (and multiplies the CTAs). Each candidate
@@ -1634,8 +1657,8 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
     auto run = [&](int t0, int nt) {
       if (nt <= 0 || ncols <= 0) return;
       dim3 grid(unsigned(nt), unsigned((ncols + cfg.bn - 1) / cfg.bn));
-      cfg.fn<<<grid, kThreadsG, cfg.smem, st>>>(*cfg.maps, H->d_tiles.as<Tile>() + t0, H->d_groups.as<Group>(),
-                                                 H->d_terms.as<Term>(), r, H->kp, cbase, ldc, cpanel, n_off);
+      launch_k(H->pdl, cfg.fn, grid, dim3(kThreadsG), cfg.smem, st, *cfg.maps, H->d_tiles.as<Tile>() + t0,
+               H->d_groups.as<Group>(), H->d_terms.as<Term>(), r, H->kp, cbase, ldc, cpanel, n_off);
     };
     // split only launches of many waves: on small trees the extra launches cost more than the
     // download they hide (config 1: 128 output tiles)
@@ -1651,8 +1674,8 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
     }
     if (L.reduce_n > 0 && !piece) {  // split term chains: segments 1.. into the group rows
       dim3 grid(unsigned(L.reduce_n), 8);
-      chain_reduce<<<grid, 256, 0, st>>>(H->d_reduces.as<ChainReduce>() + L.reduce_first,
-                                         H->d_reduce_src.as<int64_t>(), cbase, ldc, r);
+      launch_k(H->pdl, chain_reduce, grid, dim3(256), 0, st, H->d_reduces.as<ChainReduce>() + L.reduce_first,
+               H->d_reduce_src.as<int64_t>(), cbase, ldc, r);
     }
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li + 1], st));
   }

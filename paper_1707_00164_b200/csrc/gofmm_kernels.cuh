@@ -270,6 +270,13 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+// Programmatic dependent launch (host: launch_k in gofmm_capi.cu). Both are no-ops for a kernel
+// launched without the attribute.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // D(8x8) += A(8x4, row) * B(4x8, col): lane holds A[lane/4][lane%4], B[lane%4][lane/4],
 // D[lane/4][2*(lane%4) + {0,1}].
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
@@ -383,6 +390,10 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
   }
   if (threadIdx.x < 32) sTab[threadIdx.x] = exp2(double(threadIdx.x) * (1.0 / 32.0));
   __syncthreads();
+  // the plan (tiles, groups, terms, proj, coordinates) is constant; W_perm / what / c / u are
+  // written by earlier launches: let the next launch start its prologue, then wait for ours
+  pdl_launch_dependents();
+  pdl_wait();
 
   // total pipeline steps across all terms
   int total = 0;
@@ -658,6 +669,8 @@ struct ChainReduce {
 
 static __global__ void chain_reduce(const ChainReduce* __restrict__ items, const int64_t* __restrict__ src_rows,
                                     double* __restrict__ c, int64_t pstride, int32_t r) {
+  pdl_launch_dependents();
+  pdl_wait();
   const ChainReduce it = items[blockIdx.x];
   const int64_t total = int64_t(it.M) * r;
   for (int64_t e = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.y) * blockDim.x) {

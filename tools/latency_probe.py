@@ -2,7 +2,7 @@
 the CUDA-graph path (median of many, L2 flushed) and the per-launch CUDA-event times of a timed
 (non-graph) evaluation, on the product-compress tree of the config's cloud.
 
-  python tools/latency_probe.py c1 [--reps 50] [--tree compress|synth] [--mode level|dataflow]
+  python tools/latency_probe.py c1 [--reps 50] [--tree compress|synth]   (GOFMM_NO_PDL=1: no PDL)
 """
 import argparse
 import json
@@ -24,14 +24,12 @@ def main():
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--tree", default="compress")
     ap.add_argument("--precision", default="fp64")
-    ap.add_argument("--schedule", default=None, help="level | dataflow | auto (default: library choice)")
     a = ap.parse_args()
     cfg = dict(synth.CONFIGS[a.config])
     cfg["name"] = a.config
     tree, info = bench.workload_tree(cfg, cfg["n"], 0, a.tree)
     r = cfg["r"]
-    kw = {} if a.schedule is None else {"schedule": a.schedule}
-    ev = Evaluator(tree, precision=a.precision, **kw)
+    ev = Evaluator(tree, precision=a.precision)
     dt = torch.float64 if a.precision == "fp64" else torch.float32
     w = torch.randn((r, tree.n), dtype=dt, device="cuda").t()
     u = torch.empty((r, tree.n), dtype=dt, device="cuda").t()
@@ -50,7 +48,7 @@ def main():
         ms.append(e0.elapsed_time(e1))
     flops = ev.flops(r)
     med = float(np.median(ms))
-    out = {"config": a.config, "n": tree.n, "r": r, "tree": info.get("tree"), "flops": int(flops),
+    out = {"config": a.config, "pdl": os.environ.get("GOFMM_NO_PDL", "0") != "1", "n": tree.n, "r": r, "tree": info.get("tree"), "flops": int(flops),
            "graph_ms_median": round(med, 4), "graph_ms_min": round(float(np.min(ms)), 4),
            "tflops": round(flops / med / 1e9, 3), "launches_per_eval": ev.launches_per_eval,
            "near_pairs": int(len(tree.near_a)), "far_pairs": int(len(tree.far_a)), "depth": int(tree.depth)}
