@@ -403,13 +403,16 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
     // =========================== PRODUCER WARPGROUP ===========================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
     const int pth = threadIdx.x;
+    // the current term lives in registers: the term table is read once per term, at the term
+    // boundary (overlapping the next empty-slot wait), never once per stage
     int pt = grp.tbeg, pk = 0;
     while (pt < grp.tend && terms[pt].K == 0) ++pt;
+    Term T{};
+    if (pt < grp.tend) T = terms[pt];
     for (int s = 0; s < total; ++s) {
       const int stage = s % STAGES;
       const uint32_t full = smem_u32(&bars[stage]);
       mbar_wait(smem_u32(&bars[STAGES + stage]), ((s / STAGES) & 1) ^ 1);
-      const Term T = terms[pt];
       const int k0 = pk;
       if (pth == 0) {
         mbar_arrive_expect_tx(full, S::B_STAGE_BYTES);
@@ -456,6 +459,7 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
         pk = 0;
         ++pt;
         while (pt < grp.tend && terms[pt].K == 0) ++pt;
+        if (pt < grp.tend) T = terms[pt];
       }
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");  // never exit with copies in flight
@@ -542,35 +546,48 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
 #pragma unroll
   for (int ks = 0; ks < kBK / 4; ++ks) boff[ks] = swz128(wn0 + g, kpi(ks, tig));
 
-  auto advance = [&](int& t, int& k) {
-    k += kBK;
-    if (k >= terms[t].K) {
-      k = 0;
-      ++t;
-      while (t < grp.tend && terms[t].K == 0) ++t;
+  // pipeline position (term t, k offset) with the term's K and flags cached in registers: the
+  // term table is read once per term boundary, not once per stage
+  struct Pos {
+    int t, k, K, flags;
+  };
+  auto advance = [&](Pos& p) {
+    p.k += kBK;
+    if (p.k >= p.K) {
+      p.k = 0;
+      ++p.t;
+      while (p.t < grp.tend && terms[p.t].K == 0) ++p.t;
+      if (p.t < grp.tend) {
+        p.K = terms[p.t].K;
+        p.flags = terms[p.t].flags;
+      }
     }
   };
-  int ct = grp.tbeg, ck = 0;
-  while (ct < grp.tend && terms[ct].K == 0) ++ct;
+  Pos cur{grp.tbeg, 0, 0, 0};
+  while (cur.t < grp.tend && terms[cur.t].K == 0) ++cur.t;
+  if (cur.t < grp.tend) {
+    cur.K = terms[cur.t].K;
+    cur.flags = terms[cur.t].flags;
+  }
   // Stage s+1 is waited for (and, if generated, generated) while stage s is multiplied; a
   // generated tile is published through the stage's `gen` mbarrier (one arrival per consumer
   // warp), so warps only wait for each other when one falls a whole stage behind.
-  auto stage_in = [&](int s, int t, int k) {
+  auto stage_in = [&](int s, const Pos& p) {
     mbar_wait(smem_u32(&bars[s % STAGES]), (s / STAGES) & 1);
     if constexpr (kGen) {
-      if (terms[t].flags & kTermGen) generate(s, k, terms[t].K);
+      if (p.flags & kTermGen) generate(s, p.k, p.K);
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&bars[2 * STAGES + s % STAGES]));
     }
   };
-  if (total > 0) stage_in(0, ct, ck);
+  if (total > 0) stage_in(0, cur);
 #pragma unroll 1
   for (int s = 0; s < total; ++s) {
     const int stage = s % STAGES;
-    const int flags = terms[ct].flags;
-    int nt = ct, nk = ck;
-    advance(nt, nk);
-    if (s + 1 < total) stage_in(s + 1, nt, nk);
+    const int flags = cur.flags;
+    Pos nxt = cur;
+    advance(nxt);
+    if (s + 1 < total) stage_in(s + 1, nxt);
     if constexpr (kGen) mbar_wait(smem_u32(&bars[2 * STAGES + stage]), (s / STAGES) & 1);
     const bool rowA = (flags & (kTermRowMajorA | kTermGen)) != 0;  // generated tiles are row-major
     const uint32_t tA = sA_u + stage * S::A_STAGE * 8;
@@ -593,8 +610,7 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&bars[STAGES + stage]));
-    ct = nt;
-    ck = nk;
+    cur = nxt;
   }
 
   // epilogue: registers -> C; what / c in 16-row panels (crow is 16-aligned), u_perm column-major
