@@ -35,7 +35,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 FP64_PEAK_FILE = os.path.join(HERE, "profiles", "r01_fp64_peak.json")
-NCU_SUMMARY_FILE = os.path.join(HERE, "profiles", "r01_ncu_summary.json")
+NCU_SUMMARY_FILE = os.path.join(HERE, "profiles", "r02_ncu_summary.json")
 
 
 def tf32x3_peak_tflops() -> tuple[float, str]:
@@ -404,11 +404,21 @@ def ours_arm(args, world, rank, local):
             nsum = json.load(f)
         for rec in nsum.get("launches", []):
             if (rec.get("config") == args.config and rec.get("phase") == dom["phase"]
-                    and rec.get("precision", "fp64") == args.precision
+                    and rec.get("precision", "fp64") == args.precision and rec.get("tree", "synth") == args.tree
                     and rec.get("level") == dom["level"] and rec.get("n") == tree.n and rec.get("r") == r):
                 traffic = rec.get("dram_bytes")
     except Exception:
         pass
+
+    # algorithmic bytes of the dominant launch (each operand once): output launch = W_perm read +
+    # u written + the leaves' c and proj read; a downward / upward launch = its level's B rows
+    # (what / c / W_perm) and outputs plus the proj it reads — leaf-level figures from the tree
+    alg_bytes = None
+    if dom["phase"] == "output":
+        lv = np.flatnonzero(np.asarray(tree.left) < 0)
+        rk = np.maximum(np.asarray(tree.rank)[lv], 0).astype(np.int64)
+        cnt = (np.asarray(tree.end) - np.asarray(tree.start))[lv].astype(np.int64)
+        alg_bytes = int(esz * (2 * tree.n * r + int(rk.sum()) * r + int((rk * cnt).sum())))
 
     # the BASELINE metric's "rel. error" on the timed tree itself: the reference's error_eps2
     # (evaluate.hpp:330-373; r = 1, 100 sampled rows, the reference Rng draws) computed by the
@@ -512,6 +522,7 @@ def ours_arm(args, world, rank, local):
         "eps2_timed_tree": eps2,
         "phase_ms": {k: round(v[1], 3) for k, v in phases.items()} | {"permute": round(ph["ms_permute"], 3)},
         "roofline": {"bound": "tensor", "kernel": dom_name, "achieved": round(achieved, 3),
+                     "algorithmic_bytes": alg_bytes,
                      "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "peak_source": peak_src, "launch_ms": round(dom["ms"], 3), "launch_flops": int(dom["flops"]),
                      "share_of_step": round(dom["ms"] / ms, 4)},

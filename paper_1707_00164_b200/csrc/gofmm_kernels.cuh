@@ -261,6 +261,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Producer-side wait for a free slot: the consumers hold it for a whole stage of DMMAs, so the
+// waiting thread suspends (time hint) instead of spinning on the issue slots the consumers use.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity), "r"(1000000)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
                                             int32_t c2, uint32_t bar) {
   asm volatile(
@@ -320,7 +333,7 @@ struct GemmShape {
   static_assert((BM * kBK) % kConsumerThreads == 0 && kConsumerThreads % BM == 0, "generation mapping");
   static constexpr size_t smem_bytes = 1024 /* alignment slack */ + size_t(STAGES) * B_STAGE_BYTES +
                                        size_t(STAGES) * A_STAGE * 8 + size_t(STAGES) * X_STAGE * 8 +
-                                       size_t(3 * STAGES) * 8 + 32 * 8 /* exp table */ +
+                                       size_t(4 * STAGES) * 8 + 32 * 8 /* exp table */ +
                                        size_t(BM) * XD * 8 /* row coordinates */;
 };
 
@@ -366,10 +379,11 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
   unsigned char* sB = base;                                                  // [STAGES][BN*128B]
   double* sA = reinterpret_cast<double*>(sB + STAGES * S::B_STAGE_BYTES);    // [STAGES][A_STAGE]
   double* sX = sA + STAGES * S::A_STAGE;                                     // [STAGES][BK][XD]
-  // full[STAGES] (producer -> consumers), empty[STAGES] (consumers -> producer),
-  // gen[STAGES] (consumers -> consumers: generated A tile of the stage is complete)
+  // full[STAGES] (B tile, TMA -> consumers), empty[STAGES] (consumers -> producer),
+  // gen[STAGES] (consumers -> consumers: generated A tile of the stage is complete),
+  // afull[STAGES] (stored A tile / column coordinates, producer cp.async -> consumers)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sX + STAGES * S::X_STAGE);
-  double* sTab = reinterpret_cast<double*>(bars + 3 * STAGES);               // 2^(j/32), j < 32
+  double* sTab = reinterpret_cast<double*>(bars + 4 * STAGES);               // 2^(j/32), j < 32
   double* sXr = sTab + 32;                                                   // [BM][XD] row coordinates
 
   const Tile tile = tiles[blockIdx.x];
@@ -382,9 +396,10 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(smem_u32(&bars[s]), kProducerThreads + 1);  // producer arrivals + 1 expect_tx
+      mbar_init(smem_u32(&bars[s]), 1);                              // B tile: 1 expect_tx (TMA)
       mbar_init(smem_u32(&bars[STAGES + s]), kConsumerWarps);
       mbar_init(smem_u32(&bars[2 * STAGES + s]), kConsumerWarps);
+      mbar_init(smem_u32(&bars[3 * STAGES + s]), kProducerThreads);  // A tile / coordinates (cp.async)
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -412,7 +427,8 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
     for (int s = 0; s < total; ++s) {
       const int stage = s % STAGES;
       const uint32_t full = smem_u32(&bars[stage]);
-      mbar_wait(smem_u32(&bars[STAGES + stage]), ((s / STAGES) & 1) ^ 1);
+      const uint32_t afull = smem_u32(&bars[3 * STAGES + stage]);
+      mbar_wait_sleep(smem_u32(&bars[STAGES + stage]), ((s / STAGES) & 1) ^ 1);
       const int k0 = pk;
       if (pth == 0) {
         mbar_arrive_expect_tx(full, S::B_STAGE_BYTES);
@@ -453,7 +469,7 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
                      v ? src0 + mc + size_t(kk) * T.lda : T.a, v);
         }
       }
-      mbar_cp_async_arrive(full);
+      mbar_cp_async_arrive(afull);
       pk += kBK;
       if (pk >= T.K) {
         pk = 0;
@@ -572,8 +588,11 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
   // Stage s+1 is waited for (and, if generated, generated) while stage s is multiplied; a
   // generated tile is published through the stage's `gen` mbarrier (one arrival per consumer
   // warp), so warps only wait for each other when one falls a whole stage behind.
+  // Two barriers per stage: `afull` (stored A tile / column coordinates, cp.async) and `full`
+  // (the B tile, TMA). Generating stage s+1 needs only its coordinates, so the warps do not wait
+  // for stage s+1's B tile before multiplying stage s: B keeps a whole extra stage of lead.
   auto stage_in = [&](int s, const Pos& p) {
-    mbar_wait(smem_u32(&bars[s % STAGES]), (s / STAGES) & 1);
+    mbar_wait(smem_u32(&bars[3 * STAGES + s % STAGES]), (s / STAGES) & 1);
     if constexpr (kGen) {
       if (p.flags & kTermGen) generate(s, p.k, p.K);
       __syncwarp();
@@ -588,6 +607,7 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
     Pos nxt = cur;
     advance(nxt);
     if (s + 1 < total) stage_in(s + 1, nxt);
+    mbar_wait(smem_u32(&bars[stage]), (s / STAGES) & 1);
     if constexpr (kGen) mbar_wait(smem_u32(&bars[2 * STAGES + stage]), (s / STAGES) & 1);
     const bool rowA = (flags & (kTermRowMajorA | kTermGen)) != 0;  // generated tiles are row-major
     const uint32_t tA = sA_u + stage * S::A_STAGE * 8;

@@ -18,11 +18,18 @@ ap.add_argument("--evals", type=int, default=2)
 ap.add_argument("--far-mode", type=int, default=0)
 ap.add_argument("--near-mode", type=int, default=0)
 ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
+ap.add_argument("--tree", default="synth", choices=["synth", "compress"])
 a = ap.parse_args()
 over = {"n": a.n}
 if a.budget is not None:
     over["budget"] = a.budget
-tree, cfg = synth.make_config_tree(a.config, **over)
+if a.tree == "compress":  # the product compress of the config's cloud (bench.py's timed tree)
+    import bench
+
+    cfg = dict(synth.CONFIGS[a.config], name=a.config, **over)
+    tree, _ = bench.workload_tree(cfg, cfg["n"], 0, "compress")
+else:
+    tree, cfg = synth.make_config_tree(a.config, **over)
 ev = Evaluator(tree, near_mode=a.near_mode, far_mode=a.far_mode, precision=a.precision)
 r = cfg["r"]
 dt = torch.float64 if a.precision == "fp64" else torch.float32
