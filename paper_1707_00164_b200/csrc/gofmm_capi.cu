@@ -190,6 +190,22 @@ void encode_bmap(CUtensorMap* map, const double* ptr, int64_t rows, int32_t r, i
   if (rc != CUDA_SUCCESS) throw Error(GOFMM_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(rc)));
 }
 
+// A operand of one stored-A term for TMA (kernels: kABoxRow / kABoxCol): exact extents M x K, so
+// every box column / row beyond the block reads as zero (partial m-tiles, the last k-stage).
+//   row-major A[m][k] = a[k + m*lda]: dims {K, M}, box {16, kABoxRow}, 128B swizzle
+//   column-major A[m][k] = a[m + k*lda]: dims {M, K}, box {kABoxCol, 16}, 64B swizzle
+void encode_amap(CUtensorMap* map, const double* a, int64_t lda, int M, int K, bool row_major) {
+  cuuint64_t dims[2] = {cuuint64_t(row_major ? K : M), cuuint64_t(row_major ? M : K)};
+  cuuint64_t strides[1] = {cuuint64_t(lda) * sizeof(double)};
+  cuuint32_t box[2] = {row_major ? 16u : cuuint32_t(kABoxCol), row_major ? cuuint32_t(kABoxRow) : 16u};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult rc = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(a), dims, strides,
+                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                     row_major ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) throw Error(GOFMM_ERR_CUDA, "cuTensorMapEncodeTiled (A) failed: " + std::to_string(int(rc)));
+}
+
 template <int KIND, int DIM>
 void launch_generate(const double* xr, int rows, const double* xc, int cols, double* out, int64_t ld,
                      const KernelParams& kp, cudaStream_t st) {
@@ -523,6 +539,7 @@ struct gofmm_handle {
 
   // device tree
   gofmm::DevBuf d_proj, d_diag, d_near, d_far, d_xp, d_xs, d_prow, d_iperm;
+  gofmm::DevBuf d_amaps;  // TMA descriptors of the stored-A terms (upload_plan)
   std::vector<int64_t> proj_off, diag_off, near_off, far_off;  // device blob offsets (doubles)
 
   // plan
@@ -730,6 +747,15 @@ void build_f32(gofmm_handle* H) {
   const float* xn[2] = {H->d_xpn32.as<float>(), H->d_xsn32.as<float>()};
   const int bid[4] = {kBufWp, kBufWhat, kBufC, kBufC};
   size_t ti = 0;
+  // one TMA view per stored-A term (64-byte aligned 128-byte descriptors in global memory)
+  size_t n_amaps = 0;
+  for (const HostGroup& hg : H->groups)
+    for (const HostTerm& ht : hg.terms)
+      if (ht.kind == 0 && blobs[ht.a_blob] && ht.K > 0 && hg.M > 0) ++n_amaps;
+  std::vector<CUtensorMap> amaps;
+  amaps.reserve(n_amaps);
+  H->d_amaps.alloc(std::max<size_t>(n_amaps, 1) * sizeof(CUtensorMap), false);
+  const CUtensorMap* amap_base = H->d_amaps.as<CUtensorMap>();
   for (const HostGroup& hg : H->groups) {
     Group g{};
     g.crow = hg.c_row;
@@ -1438,6 +1464,15 @@ void upload_plan(gofmm_handle* H) {
       default: return int32_t(kBufC);
     }
   };
+  // one TMA view per stored-A term (64-byte aligned 128-byte descriptors in global memory)
+  size_t n_amaps = 0;
+  for (const HostGroup& hg : H->groups)
+    for (const HostTerm& ht : hg.terms)
+      if (ht.kind == 0 && blobs[ht.a_blob] && ht.K > 0 && hg.M > 0) ++n_amaps;
+  std::vector<CUtensorMap> amaps;
+  amaps.reserve(n_amaps);
+  H->d_amaps.alloc(std::max<size_t>(n_amaps, 1) * sizeof(CUtensorMap), false);
+  const CUtensorMap* amap_base = H->d_amaps.as<CUtensorMap>();
   for (const HostGroup& hg : H->groups) {
     Group g{};
     g.crow = hg.c_row;
@@ -1456,14 +1491,21 @@ void upload_plan(gofmm_handle* H) {
         t.a = nullptr;
       } else {
         t.flags = ht.row_major ? kTermRowMajorA : 0;
-        t.a = blobs[ht.a_blob] + ht.a_off;
+        t.a = blobs[ht.a_blob] ? blobs[ht.a_blob] + ht.a_off : nullptr;
         t.lda = ht.lda;
+        if (t.a && ht.K > 0 && hg.M > 0) {
+          amaps.emplace_back();
+          encode_amap(&amaps.back(), t.a, ht.lda, hg.M, ht.K, ht.row_major);
+          t.amap = amap_base + (amaps.size() - 1);
+        }
       }
       ts.push_back(t);
     }
     g.tend = int(ts.size());
     gs.push_back(g);
   }
+  if (!amaps.empty())
+    GOFMM_CUDA(cudaMemcpy(H->d_amaps.p, amaps.data(), amaps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
   GOFMM_CUDA(cudaMemcpy(H->d_groups.p, gs.data(), gs.size() * sizeof(Group), cudaMemcpyHostToDevice));
   if (!ts.empty()) GOFMM_CUDA(cudaMemcpy(H->d_terms.p, ts.data(), ts.size() * sizeof(Term), cudaMemcpyHostToDevice));
   H->plan_uploaded = true;

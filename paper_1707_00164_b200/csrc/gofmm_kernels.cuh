@@ -33,6 +33,7 @@ enum : int32_t { kBufWp = 0, kBufWhat = 1, kBufC = 2 };
 
 struct Term {
   const double* a;   // stored A (nullptr when generated)
+  const CUtensorMap* amap;  // stored A: TMA view of this term's block (global memory, see encode_amap)
   const double* xr;  // generated: row points, point-major (dim doubles per point)
   const double* xc;  // generated: column points
   int64_t lda;
@@ -274,6 +275,17 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
       "r"(parity), "r"(1000000)
       : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
                                             int32_t c2, uint32_t bar) {
   asm volatile(
@@ -300,6 +312,10 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 
 // ------------------------------------------------------------------ grouped multi-term GEMM
 constexpr int kBK = 16;  // k-depth per stage: one 128-byte TMA row of FP64
+// Stored A tiles arrive by TMA (one tensor map per stored-A term, exact extents: partial tiles
+// read zeros). Row-major A (A[m][k] = a[k + m*lda]) in boxes of 16 k x kABoxRow m, SWIZZLE_128B;
+// column-major A (A[m][k] = a[m + k*lda]) in boxes of kABoxCol m x 16 k, SWIZZLE_64B.
+constexpr int kABoxRow = 32, kABoxCol = 8;
 
 // Warp roles: warpgroup 0 = producer (4 warps: thread 0 issues the B-tile TMA, all 128 threads
 // stage stored A tiles / point coordinates with cp.async), then 16 consumer warps (4 per SM
@@ -320,9 +336,10 @@ struct GemmShape {
   static constexpr int kThreads = kProducerThreads + kConsumerThreads;
   static constexpr int WTM = BM / WM, WTN = BN / WN;
   static constexpr int MT = WTM / 8, NT = WTN / 8;
-  static constexpr int SA_COL = BM;       // stored A column-major tile [BK][BM], XOR-swizzled chunks
-  static constexpr int SA_ROW = kBK + 2;  // row-major / generated A tile [BM][BK+2]
-  static constexpr int A_STAGE = (kBK * SA_COL > BM * SA_ROW) ? kBK * SA_COL : BM * SA_ROW;  // doubles
+  // A tile of a stage (doubles): row-major / generated [BM][16] 128B-swizzled (swz128), or
+  // column-major [BM/8][16][8] 64B-swizzled (acm64); 1024-byte aligned like the B tiles
+  static constexpr int A_STAGE = BM * kBK;
+  static_assert(BM % kABoxRow == 0 && (A_STAGE * 8) % 1024 == 0, "A tile = whole TMA boxes");
   static constexpr int B_STAGE_BYTES = BN * kBK * 8;  // TMA box, 128B-swizzled rows, 1024B aligned
   static constexpr int X_STAGE = kBK * XD;            // column coordinates (generated terms)
   static constexpr int GEN_PER_THREAD = (BM * kBK) / kConsumerThreads;
@@ -354,10 +371,11 @@ __device__ __forceinline__ uint32_t swz128(int n, int k) {
 // leaves a 2-way conflict per half-warp).
 __device__ __forceinline__ int kpi(int ks, int tig) { return 2 * ks + (tig & 1) + 8 * (tig >> 1); }
 
-// Column-major stored A tile [BK][BM]: 16-byte chunk (2 consecutive m) index XORed with 2*h(k),
-// h distinct for the four k of one sub-step, so fragment loads are conflict-free as well.
-__device__ __forceinline__ int acol_chunk(int k, int mchunk) {
-  return mchunk ^ (2 * ((k & 1) | (((k >> 3) & 1) << 1)));
+// byte offset of A(m, k) in a column-major stored A tile as TMA writes it: boxes of 8 m x 16 k
+// (1 KB each, m-box j at j*1024), rows of 64 bytes (one k), 64B swizzle (16-byte chunk ^= bits 7-8).
+__device__ __forceinline__ uint32_t acm64(int m, int k) {
+  return uint32_t(m >> 3) * 1024u + uint32_t(k) * 64u + ((uint32_t(((m & 7) >> 1) ^ ((k >> 1) & 3)) << 4) |
+                                                        (uint32_t(m & 1) << 3));
 }
 
 __device__ __forceinline__ void consumer_bar() {
@@ -447,26 +465,17 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
             cp_async8(dX + uint32_t(kk * XD + q) * 8u, v ? T.xc + size_t(k0 + kk) * dim + q : T.xc, v);
           }
         }
-      } else if (T.flags & kTermRowMajorA) {
-        // A[m][k] = a[k + m*lda]; 16-byte chunks along k
+      } else if (pth == 0) {
+        // stored A by TMA on the stage's afull barrier (its bytes are added to the phase first)
         const uint32_t dA = smem_u32(sA + stage * S::A_STAGE);
-        const double* src0 = T.a + k0 + size_t(m0) * T.lda;
-#pragma unroll 2
-        for (int c = pth; c < BM * (kBK / 2); c += kProducerThreads) {
-          const int m = c >> 3, kc = (c & 7) * 2;
-          const bool v = (m0 + m < M) && (k0 + kc < T.K);
-          cp_async16(dA + uint32_t(m * S::SA_ROW + kc) * 8u, v ? src0 + kc + size_t(m) * T.lda : T.a, v);
-        }
-      } else {
-        // A[m][k] = a[m + k*lda]; 16-byte chunks along m, chunk index swizzled per k row
-        const uint32_t dA = smem_u32(sA + stage * S::A_STAGE);
-        const double* src0 = T.a + m0 + size_t(k0) * T.lda;
-#pragma unroll 2
-        for (int c = pth; c < kBK * (BM / 2); c += kProducerThreads) {
-          const int kk = c / (BM / 2), mch = c % (BM / 2), mc = mch * 2;
-          const bool v = (m0 + mc < M) && (k0 + kk < T.K);
-          cp_async16(dA + uint32_t(kk * S::SA_COL + 2 * acol_chunk(kk, mch)) * 8u,
-                     v ? src0 + mc + size_t(kk) * T.lda : T.a, v);
+        mbar_expect_tx(afull, uint32_t(S::A_STAGE * 8));
+        if (T.flags & kTermRowMajorA) {
+#pragma unroll
+          for (int j = 0; j < BM / kABoxRow; ++j)
+            tma_load_2d(dA + uint32_t(j) * (kABoxRow * 128u), T.amap, k0, m0 + j * kABoxRow, afull);
+        } else {
+#pragma unroll
+          for (int j = 0; j < BM / kABoxCol; ++j) tma_load_2d(dA + uint32_t(j) * 1024u, T.amap, m0 + j * kABoxCol, k0, afull);
         }
       }
       mbar_cp_async_arrive(afull);
@@ -529,8 +538,7 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
             xr[q] = lds64(xrU + uint32_t(q) * 8u);
           }
         const double v = (row_ok && k0 + kk < Kt) ? kernel_entry_fast<KIND, DIM>(xr, xc, kp, tabU) : 0.0;
-        asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(tA + uint32_t(gen_m * S::SA_ROW + kk) * 8u), "d"(v)
-                     : "memory");
+        asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(tA + swz128(gen_m, kk)), "d"(v) : "memory");
       }
     }
   };
@@ -618,8 +626,7 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
 #pragma unroll
       for (int i = 0; i < S::MT; ++i) {
         const int kk = kpi(ks, tig), m = wm0 + 8 * i + g;
-        a[i] = rowA ? lds64(tA + uint32_t(m * S::SA_ROW + kk) * 8u)
-                    : lds64(tA + uint32_t(kk * S::SA_COL + 2 * acol_chunk(kk, m >> 1) + (m & 1)) * 8u);
+        a[i] = lds64(tA + (rowA ? swz128(m, kk) : acm64(m, kk)));
       }
 #pragma unroll
       for (int j = 0; j < S::NT; ++j) {
