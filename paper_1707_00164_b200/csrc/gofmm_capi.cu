@@ -206,6 +206,19 @@ void encode_amap(CUtensorMap* map, const double* a, int64_t lda, int M, int K, b
   if (rc != CUDA_SUCCESS) throw Error(GOFMM_ERR_CUDA, "cuTensorMapEncodeTiled (A) failed: " + std::to_string(int(rc)));
 }
 
+// FP32 stored A (K-major hi / lo copies, A[m][k] = a[k + m*lda]): dims {K, M}, box {16, 128}
+// (one UMMA K-major SWIZZLE_64B tile, the layout the A producers write for generated terms).
+void encode_amap32(CUtensorMap* map, const float* a, int64_t lda, int M, int K) {
+  cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(M)};
+  cuuint64_t strides[1] = {cuuint64_t(lda) * sizeof(float)};
+  cuuint32_t box[2] = {16u, 128u};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult rc = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a), dims, strides,
+                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) throw Error(GOFMM_ERR_CUDA, "cuTensorMapEncodeTiled (A32) failed: " + std::to_string(int(rc)));
+}
+
 template <int KIND, int DIM>
 void launch_generate(const double* xr, int rows, const double* xc, int cols, double* out, int64_t ld,
                      const KernelParams& kp, cudaStream_t st) {
@@ -747,11 +760,11 @@ void build_f32(gofmm_handle* H) {
   const float* xn[2] = {H->d_xpn32.as<float>(), H->d_xsn32.as<float>()};
   const int bid[4] = {kBufWp, kBufWhat, kBufC, kBufC};
   size_t ti = 0;
-  // one TMA view per stored-A term (64-byte aligned 128-byte descriptors in global memory)
+  // two TMA views (hi, lo) per stored-A term (64-byte aligned 128-byte descriptors in global memory)
   size_t n_amaps = 0;
   for (const HostGroup& hg : H->groups)
     for (const HostTerm& ht : hg.terms)
-      if (ht.kind == 0 && blobs[ht.a_blob] && ht.K > 0 && hg.M > 0) ++n_amaps;
+      if (ht.kind == 0 && ht.K > 0 && hg.M > 0) n_amaps += 2;
   std::vector<CUtensorMap> amaps;
   amaps.reserve(n_amaps);
   H->d_amaps.alloc(std::max<size_t>(n_amaps, 1) * sizeof(CUtensorMap), false);
@@ -779,6 +792,13 @@ void build_f32(gofmm_handle* H) {
         t.a_hi = H->d_a32h.as<float>() + H->term_a32_off[ti];
         t.a_lo = H->d_a32l.as<float>() + H->term_a32_off[ti];
         t.lda = H->term_a32_ld[ti];
+        if (ht.K > 0 && hg.M > 0) {
+          t.amap = amap_base + amaps.size();
+          amaps.emplace_back();
+          encode_amap32(&amaps.back(), t.a_hi, t.lda, hg.M, ht.K);
+          amaps.emplace_back();
+          encode_amap32(&amaps.back(), t.a_lo, t.lda, hg.M, ht.K);
+        }
       }
       ts.push_back(t);
       ++ti;
@@ -786,6 +806,8 @@ void build_f32(gofmm_handle* H) {
     g.tend = int(ts.size());
     gs.push_back(g);
   }
+  if (!amaps.empty())
+    GOFMM_CUDA(cudaMemcpy(H->d_amaps.p, amaps.data(), amaps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
   H->d_groups.upload(gs);
   H->d_terms32.upload(ts.empty() ? std::vector<f32::Term>(1) : ts);
   // the FP64 operand blobs are not read by an FP32 handle

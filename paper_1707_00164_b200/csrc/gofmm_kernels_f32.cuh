@@ -36,6 +36,7 @@ namespace f32 {
 struct Term {
   const float* a_hi;  // stored A, K-major: A[m][k] = a[k + m*lda] (lda multiple of 4)
   const float* a_lo;
+  const CUtensorMap* amap;  // stored A: TMA views of a_hi, a_lo (two consecutive maps)
   const float* xr;  // generated: row points (point-major FP32, `dim` floats per point)
   const float* xc;  // generated: column points
   const float* xrn;  // Gaussian: -log2(e)/(2h^2) |x|^2 of the row / column points (from FP64)
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(bar_full_a(s), kAThreads / 32);
+      mbar_init(bar_full_a(s), kAThreads / 32 + 1);  // A-producer warps + the TMA thread
       mbar_init(bar_full_b(s), 1);
       mbar_init(bar_empty(s), 1);
     }
@@ -285,11 +286,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       int t = first_term(), k = 0;
       struct {
         const float *xc, *xcn;
+        const CUtensorMap* amap;
         int64_t b_row;
         int32_t K, flags, bbuf;
       } T{};
       auto load_term = [&]() {
         if (t < grp.tend) {
+          T.amap = terms[t].amap;
           T.xc = terms[t].xc;
           T.xcn = terms[t].xcn;
           T.b_row = terms[t].b_row;
@@ -323,6 +326,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                   x_tile(st) + uint32_t(kBK * (kMaxDimRt + 1) * 4)),
               "l"(T.xcn + k), "r"(nbytes), "r"(bar_full_b(st))
               : "memory");
+        // stored A (hi, lo): TMA into the stage's A tiles on full_a (exact extents: rows past M and
+        // k past K read zero); a generated stage's A is written by the producer warps instead
+        if (!gen) {
+          mbar_arrive_expect_tx(bar_full_a(st), 2 * kATileBytes);
+          tma_load_2d(a_tile(st, 0), T.amap, k, m0, bar_full_a(st));
+          tma_load_2d(a_tile(st, 1), T.amap + 1, k, m0, bar_full_a(st));
+        } else {
+          mbar_arrive(bar_full_a(st));
+        }
         k += kBK;
         if (k >= T.K) {
           k = 0;
@@ -413,20 +425,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     int t = first_term(), k = 0;
     // current term in registers (see the TMA thread): K, flags and the stored-A operand
     int tK = 0, tFlags = 0;
-    const float* tAh = nullptr;
-    const float* tAl = nullptr;
-    int64_t tLda = 0;
     auto load_term = [&]() {
       if (t < grp.tend) {
         tK = terms[t].K;
         tFlags = terms[t].flags;
-        tAh = terms[t].a_hi;
-        tAl = terms[t].a_lo;
-        tLda = terms[t].lda;
       }
     };
     load_term();
-    int pending = -1;  // stage whose cp.async copies are still in flight (arrival deferred by one)
     auto arrive = [&](int st) {
       fence_proxy_async();  // generic-proxy writes -> visible to the tensor core (async proxy)
       __syncwarp();
@@ -504,28 +509,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           sts128(dl + sw64(m, 2 * h), lo[0], lo[1], lo[2], lo[3]);
           sts128(dl + sw64(m, 2 * h + 1), lo[4], lo[5], lo[6], lo[7]);
         }
-        if (pending >= 0) {
-          asm volatile("cp.async.wait_all;\n" ::: "memory");
-          arrive(pending);
-          pending = -1;
-        }
         arrive(st);
       } else {
-        // stored K-major A: rows m0+m, k .. k+15 of this term; 16-byte chunks (4 floats)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int kc = k + 8 * h + 4 * c;
-          const bool v = row_ok && kc < tK;
-          const size_t off = size_t(m0 + m) * tLda + kc;
-          cp_async16(dh + sw64(m, 2 * h + c), v ? tAh + off : tAh, v);
-          cp_async16(dl + sw64(m, 2 * h + c), v ? tAl + off : tAl, v);
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-        if (pending >= 0) {
-          asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-          arrive(pending);
-        }
-        pending = st;
+        // stored A arrives by TMA (the TMA thread); this warp only marks the stage
+        arrive(st);
       }
       k += kBK;
       if (k >= tK) {
@@ -534,10 +521,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (t < grp.tend && terms[t].K == 0) ++t;
         load_term();
       }
-    }
-    if (pending >= 0) {
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
-      arrive(pending);
     }
 
     // =========================== EPILOGUE: registers -> C ===========================
