@@ -23,8 +23,15 @@ ap.add_argument("--config", default="c3")
 ap.add_argument("--ranks", default="2,4,8")
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--busbw", type=float, default=650.0)
+ap.add_argument("--tree", default="compress", choices=["compress", "synth"])
 a = ap.parse_args()
-tree, cfg = synth.make_config_tree(a.config)
+if a.tree == "compress":  # bench.py's timed tree: the product compress of the config's cloud
+    import bench
+
+    cfg = dict(synth.CONFIGS[a.config], name=a.config)
+    tree, _ = bench.workload_tree(cfg, cfg["n"], 0, "compress")
+else:
+    tree, cfg = synth.make_config_tree(a.config)
 r = cfg["r"]
 w = torch.randn((r, tree.n), dtype=torch.float64, device="cuda").t()
 u = torch.zeros((r, tree.n), dtype=torch.float64, device="cuda").t()
@@ -46,7 +53,7 @@ def timed(fn):
 with Evaluator(tree) as ev:
     t1 = timed(lambda: ev.evaluate_torch(w, out=u))
     flops = ev.flops(r)
-out = {"config": a.config, "n": tree.n, "r": r, "t1_ms": round(t1, 3), "busbw_gbs_assumed": a.busbw, "ranks": {}}
+out = {"config": a.config, "tree": a.tree, "n": tree.n, "r": r, "t1_ms": round(t1, 3), "busbw_gbs_assumed": a.busbw, "ranks": {}}
 for P in [int(x) for x in a.ranks.split(",")]:
     s1, s2, slot = [], [], 0
     for g in range(P):
