@@ -237,6 +237,12 @@ int gofmm_dist_evaluate(gofmm_handle* h, const double* d_w, int64_t ldw, int32_t
 int gofmm_dist_evaluate_f32(gofmm_handle* h, const float* d_w, int64_t ldw, int32_t r, float* d_u_perm,
                             int64_t ldu, void* stream, int32_t timed, double* ms3);
 
+/* The same with HOST buffers: W (n x r, original order) is uploaded, the evaluation above runs on
+ * the handle's stream, and this rank's rows [own_row_begin, own_row_end) of u_perm are written back
+ * (other rows are not touched). Synchronous; ms3 may be NULL (else timed as above). */
+int gofmm_dist_evaluate_host(gofmm_handle* h, const double* w, int64_t ldw, int32_t r, double* u_perm, int64_t ldu,
+                             double* ms3);
+
 /* FP32 handles: the same two stages; the send buffer is 2 * max_send_rows * r floats (hi then
  * lo halves of the 3xTF32 operands), recv is nranks of those slots in rank order. */
 int gofmm_dist_stage1_f32(gofmm_handle* h, const float* d_w, int64_t ldw, int32_t r, float* d_send, void* stream);

@@ -22,9 +22,12 @@
 //   B200Evaluator(h, &points, GOFMM_KERNEL_POLYNOMIAL, c, degree)   Polynomial oracle.hpp:197-219
 //   B200Evaluator(h, &points, GOFMM_KERNEL_EXPONENTIAL, h)          Matern-1/2 (BASELINE config 4)
 //   B200Evaluator::matrix_free(h, laplace_oracle)                   from the oracle object itself
+// Multi-GPU (one process per GPU): B200Evaluator::distributed(h, &points, kernel, p0, p1, rank,
+// nranks) + init_comm(id) + evaluate_dist(w) — this rank's rows of u (gofmm_dist_evaluate_host).
 #ifndef GOFMM_B200_GFMM_HPP
 #define GOFMM_B200_GFMM_HPP
 
+#include <chrono>
 #include <cmath>
 #include <map>
 #include <memory>
@@ -52,6 +55,52 @@ class B200Evaluator {
                 int device = 0) {
     if (!points) throw std::invalid_argument("matrix-free evaluation needs the point cloud");
     build(h, points, kernel, p0, p1, device);
+  }
+  /// One rank of the subtree-split evaluation over nranks GPUs (north_star (4)),
+  /// matrix-free from the point coordinates. Every rank builds it from the same HMatrix; rank 0 gets
+  /// a unique id from nccl_unique_id(), the caller broadcasts it (e.g. MPI_Bcast) and every rank
+  /// calls init_comm(id) — then evaluate_dist(w) on every rank, once per evaluation.
+  static std::unique_ptr<B200Evaluator> distributed(const HMatrix& h, const PointCloud* points, int kernel, double p0,
+                                                    double p1, int rank, int nranks, int device = 0) {
+    if (!points) throw std::invalid_argument("distributed evaluation needs the point cloud");
+    std::unique_ptr<B200Evaluator> ev(new B200Evaluator());
+    ev->build(h, points, kernel, p0, p1, device, rank, nranks);
+    return ev;
+  }
+  static std::vector<unsigned char> nccl_unique_id() {
+    std::vector<unsigned char> id(GOFMM_NCCL_UNIQUE_ID_BYTES);
+    if (gofmm_nccl_unique_id(id.data()) != GOFMM_OK)
+      throw std::runtime_error(std::string("gofmm_nccl_unique_id: ") + gofmm_last_error());
+    return id;
+  }
+  /// Collective over the nranks processes (ncclCommInitRank); not needed for a single rank.
+  void init_comm(const void* unique_id) {
+    if (gofmm_dist_init_comm(h_, unique_id) != GOFMM_OK)
+      throw std::runtime_error(std::string("gofmm_dist_init_comm: ") + gofmm_last_error());
+  }
+  /// This rank's permuted rows [first, second) of u.
+  std::pair<int64_t, int64_t> own_rows() const {
+    gofmm_dist_info info{};
+    if (gofmm_dist_get_info(h_, &info) != GOFMM_OK) throw std::runtime_error(gofmm_last_error());
+    return {info.own_row_begin, info.own_row_end};
+  }
+  /// evaluate() of this rank's share: W (full, original order) in, u_perm with this rank's rows
+  /// [own_rows()) filled (zeros elsewhere); flops = this rank's reference-counted share.
+  Potentials evaluate_dist(const Matrix& w) const {
+    if (w.rows() != n_) throw std::invalid_argument("evaluate: w has wrong row count");
+    if (w.cols() < 1) throw std::invalid_argument("evaluate: w needs at least one column");
+    Potentials p;
+    p.u = Matrix::Zero(w.rows(), w.cols());
+    const auto t0 = std::chrono::steady_clock::now();
+    const int rc = gofmm_dist_evaluate_host(h_, w.data(), w.rows(), static_cast<int32_t>(w.cols()), p.u.data(),
+                                            p.u.rows(), nullptr);
+    if (rc == GOFMM_ERR_INVALID) throw std::invalid_argument(gofmm_last_error());
+    if (rc != GOFMM_OK) throw std::runtime_error(std::string("gofmm_dist_evaluate_host: ") + gofmm_last_error());
+    gofmm_dist_info info{};
+    gofmm_dist_get_info(h_, &info);
+    p.flops = info.flops_per_rhs * w.cols();
+    p.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return p;
   }
   /// Matrix-free from the reference oracle object (its points and parameter).
   static std::unique_ptr<B200Evaluator> matrix_free(const HMatrix& h, const LaplaceKernelOracle& k, int device = 0) {
@@ -82,7 +131,9 @@ class B200Evaluator {
   }
 
  private:
-  void build(const HMatrix& h, const PointCloud* pts, int kernel, double p0, double p1, int device) {
+  B200Evaluator() = default;
+  void build(const HMatrix& h, const PointCloud* pts, int kernel, double p0, double p1, int device, int rank = 0,
+             int nranks = 0) {
     const MetricTree& t = h.tree;
     n_ = h.n;
     const int nn = static_cast<int>(t.nodes.size());
@@ -167,7 +218,7 @@ class B200Evaluator {
     }
     gofmm_options o{};
     o.device = device;
-    const int rc = gofmm_create(&d, &o, &h_);
+    const int rc = nranks > 0 ? gofmm_create_dist(&d, &o, rank, nranks, &h_) : gofmm_create(&d, &o, &h_);
     if (rc == GOFMM_ERR_INVALID) throw std::invalid_argument(gofmm_last_error());
     if (rc != GOFMM_OK) throw std::runtime_error(std::string("gofmm_create: ") + gofmm_last_error());
   }

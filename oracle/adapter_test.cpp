@@ -103,6 +103,18 @@ int main(int argc, char** argv) {
   check("stored evaluator", rel2(g1.u, ref.u) <= 1e-12 && g1.flops == ref.flops);
   check("matrix-free gaussian", rel2(g2.u, ref.u) <= 1e-12 && g2.flops == ref.flops);
 
+  // --- the distributed evaluator's data plane on a single rank (no communicator needed): the
+  // subtree-split stages + the in-library exchange path, every row owned
+  {
+    auto d1 = B200Evaluator::distributed(h, &pc, GOFMM_KERNEL_GAUSSIAN, 1.0, 0.0, 0, 1);
+    const auto rows = d1->own_rows();
+    const Potentials pd = d1->evaluate_dist(w);
+    std::printf("distributed(1 rank) rows=[%lld,%lld) rel=%.3e flops=%lld\n", (long long)rows.first,
+                (long long)rows.second, rel2(pd.u, ref.u), (long long)pd.flops);
+    check("distributed evaluator, 1 rank", rows.first == 0 && rows.second == n && rel2(pd.u, ref.u) <= 1e-12 &&
+                                               pd.flops == ref.flops);
+  }
+
   // --- error_eps2 routed to the GPU
   const ErrorReport e_ref = error_eps2(h, K, 2, 100, 42);
   const ErrorReport e_gpu = error_eps2_b200(h, K, 2, 100, 42);

@@ -146,7 +146,7 @@ EXPORTS = ("gofmm_create", "gofmm_evaluate", "gofmm_evaluate_device", "gofmm_unp
            "gofmm_dist_attach_comm", "gofmm_dist_evaluate", "gofmm_dist_evaluate_f32", "gofmm_compress_default_config",
            "gofmm_compress", "gofmm_compressed_desc", "gofmm_compressed_stats", "gofmm_compressed_free",
            "gofmm_compress_last_error", "gofmm_error_eps2", "gofmm_points_gaussian",
-           "gofmm_default_laplace_floor", "gofmm_rng_gauss_stream")
+           "gofmm_default_laplace_floor", "gofmm_rng_gauss_stream", "gofmm_dist_evaluate_host")
 
 
 class Eps2Report(C.Structure):
@@ -194,6 +194,7 @@ def lib():
         L.gofmm_dist_init_comm.argtypes = [P, P]
         L.gofmm_dist_attach_comm.argtypes = [P, P]
         L.gofmm_dist_evaluate.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, P, C.c_int32, P]
+        L.gofmm_dist_evaluate_host.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, P]
         L.gofmm_dist_evaluate_f32.argtypes = [P, P, C.c_int64, C.c_int32, P, C.c_int64, P, C.c_int32, P]
         L.gofmm_error_eps2.argtypes = [P, C.c_int32, C.c_int32, C.c_uint64, C.POINTER(Eps2Report), P]
         L.gofmm_points_gaussian.argtypes = [C.c_int32, C.c_int32, C.c_uint64, P]

@@ -2300,6 +2300,35 @@ int dist_evaluate_entry(gofmm_handle* H, const T* d_w, int64_t ldw, int32_t r, T
 
 extern "C" {
 
+// Host buffers (the drop-in form of one rank's evaluation, e.g. the C++ adapter's
+// B200Evaluator::evaluate_dist): W (full, original order) is uploaded, the in-library data plane runs,
+// and this rank's rows [own_row_begin, own_row_end) of u_perm are downloaded; other rows untouched.
+int gofmm_dist_evaluate_host(gofmm_handle* H, const double* w, int64_t ldw, int32_t r, double* u_perm, int64_t ldu,
+                             double* ms3) {
+  return guarded([&] {
+    check_args(H, w, ldw, r, u_perm, ldu);
+    check_precision(H, GOFMM_PRECISION_F64);
+    std::lock_guard<std::mutex> lk(H->mu);
+    GOFMM_CUDA(cudaSetDevice(H->device));
+    cudaStream_t st = H->stream;
+    DevBuf dw, du;
+    dw.alloc(size_t(H->n) * r * sizeof(double), false);
+    du.alloc(size_t(H->n) * r * sizeof(double), false);
+    GOFMM_CUDA(cudaMemcpy2DAsync(dw.p, size_t(H->n) * sizeof(double), w, size_t(ldw) * sizeof(double),
+                                 size_t(H->n) * sizeof(double), size_t(r), cudaMemcpyHostToDevice, st));
+    {
+      WsGuard ws(H, st);
+      dist_evaluate<double>(H, dw.as<double>(), H->n, r, du.as<double>(), H->n, st, ms3 != nullptr, ms3);
+    }
+    const int64_t b = H->own_begin, e = H->own_end;
+    if (e > b)
+      GOFMM_CUDA(cudaMemcpy2DAsync(u_perm + b, size_t(ldu) * sizeof(double), du.as<double>() + b,
+                                   size_t(H->n) * sizeof(double), size_t(e - b) * sizeof(double), size_t(r),
+                                   cudaMemcpyDeviceToHost, st));
+    GOFMM_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 int gofmm_nccl_unique_id(void* id_out) {
   return guarded([&] {
     if (!id_out) throw Error(GOFMM_ERR_INVALID, "null unique id buffer");

@@ -3,7 +3,8 @@ the reference headers into oracle/_ref/adapter_test (oracle/Makefile, target `ad
 reference's own compress() + evaluate() + error_eps2() next to the adapter on the same HMatrix —
 gfmm::evaluate_b200(h, w, opts) (evaluate()'s signature, cached per HMatrix), the stored and the
 matrix-free evaluators (Gaussian, Laplace, Exponential) within 1e-12 with equal flop counters,
-error_eps2_b200 == error_eps2, 4 threads calling evaluate_b200 on one HMatrix concurrently
+error_eps2_b200 == error_eps2, the distributed evaluator (B200Evaluator::distributed +
+evaluate_dist over gofmm_dist_evaluate_host) on one rank, 4 threads calling evaluate_b200 on one HMatrix concurrently
 bitwise equal to serial calls (SPEC.md:429), and std::invalid_argument on a wrong-sized W
 (evaluate.hpp:288-289)."""
 import os
