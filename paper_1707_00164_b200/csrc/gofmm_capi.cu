@@ -119,6 +119,8 @@ constexpr int kStagesGW = 3, kBM_GW = 32, kBN_GW = 512;
 // SN64: stored operands for r <= 64 (64x64 tiles: twice the CTAs of S, no idle columns)
 #define CFG_SN64 kBM_G, 64, 4, 4, kStagesS
 constexpr int kBM[3] = {kBM_S, kBM_G, kBM_GW};  // tile-row classes of the FP64 tile lists
+// per-CTA fixed cost in the launch-config model, in tile-area x k-stage units (one 128x128 stage)
+constexpr double kCtaOverheadArea = double(kBM_S) * kBN_S / 0.8;
 constexpr int kThreadsG = kProducerThreads + kConsumerThreads;  // every FP64 config: producer WG + 16 consumer warps
 
 using KernelFn = void (*)(BMaps, const Tile*, const Group*, const Term*, int32_t, KernelParams, double*, int64_t,
@@ -604,6 +606,8 @@ struct gofmm_handle {
   gofmm::f32::BMaps maps32{};
   int32_t maps32_r = 0;
 
+  gofmm::KernelFn kfn_sw = nullptr, kfn_sg = nullptr;
+  size_t smem_sw = 0, smem_sg = 0;
   gofmm::KernelFn kfn_s = nullptr, kfn_sn64 = nullptr, kfn_g = nullptr, kfn_gw = nullptr, kfn_gn64 = nullptr,
                   kfn_gn128 = nullptr, kfn_gn64w = nullptr;
   size_t smem_s = 0, smem_sn64 = 0, smem_g = 0, smem_gw = 0, smem_gn64 = 0, smem_gn128 = 0, smem_gn64w = 0;
@@ -1406,6 +1410,13 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_s)));
   H->kfn_sn64 = &grouped_gemm_f64<CFG_SN64, kKindNone, 1>;
   H->smem_sn64 = gemm_smem_bytes<CFG_SN64, kKindNone, 1>();
+  // skinny stored GEMMs (N2S of low-rank nodes: M = k << 128): the wide tiles' few, long CTAs
+  H->kfn_sw = &grouped_gemm_f64<CFG_GW, kKindNone, 1>;
+  H->smem_sw = gemm_smem_bytes<CFG_GW, kKindNone, 1>();
+  GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_sw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_sw)));
+  H->kfn_sg = &grouped_gemm_f64<CFG_G, kKindNone, 1>;
+  H->smem_sg = gemm_smem_bytes<CFG_G, kKindNone, 1>();
+  GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_sg, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_sg)));
   GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_sn64, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_sn64)));
   if (!stored && (gen_near || gen_far)) {
     GenKernel gk = pick_gen_kernel(H->kernel, H->dim);
@@ -1615,9 +1626,11 @@ LaunchCfg pick_launch_cfg(const gofmm_handle* H, const Launch& L, int32_t r) {
     int bm;
     double eff;  // achieved fraction of the DMMA peak when the SMs are full (measured, rounded)
   };
-  Cand c[5];
+  Cand c[6];
   int nc = 0;
   if (!L.gen) {
+    if (use_wide(r)) c[nc++] = {{H->kfn_sw, H->smem_sw, kBN_GW, &H->maps_g, 2}, kBM_GW, 0.80};
+    if (r > 128) c[nc++] = {{H->kfn_sg, H->smem_sg, kBN_G, &H->maps_g, 1}, kBM_G, 0.78};
     if (r > 64) c[nc++] = {{H->kfn_s, H->smem_s, kBN_S, &H->maps_s, 0}, kBM_S, 0.80};
     c[nc++] = {{H->kfn_sn64, H->smem_sn64, 64, &H->maps_n64, 1}, kBM_G, 0.60};
   } else {
@@ -1632,7 +1645,11 @@ LaunchCfg pick_launch_cfg(const gofmm_handle* H, const Launch& L, int32_t r) {
   for (int i = 0; i < nc; ++i) {
     const int nt = (r + c[i].cfg.bn - 1) / c[i].cfg.bn;
     const double work = double(L.chain_sum[c[i].cfg.bm_class]) * nt / double(H->num_sms);
-    const double t = double(c[i].bm) * c[i].cfg.bn / c[i].eff * std::max(work, double(L.chain_max));
+    // + a fixed cost per CTA (prologue, pipeline fill, epilogue ~ one 128x128 k-stage): launches of
+    // many short chains (N2S of low-rank leaves: 1-3 stages per tile) are bound by it, not by math
+    const double ctas = double(L.tn[c[i].cfg.bm_class]) * nt / double(H->num_sms);
+    const double t = double(c[i].bm) * c[i].cfg.bn / c[i].eff * std::max(work, double(L.chain_max)) +
+                     kCtaOverheadArea * ctas;
     if (i == 0 || t < best_t) {
       best = i;
       best_t = t;
@@ -1686,7 +1703,7 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
     const int64_t row0 = 0, row1 = H->ld_wp;
     const int32_t pc0 = piece ? c0 : 0, pr = piece ? c1 - c0 : r;  // columns of this piece
     if (row1 > row0 && pr > 0) {
-      dim3 grid(unsigned((row1 - row0 + 255) / 256), unsigned((pr + cpb - 1) / cpb));
+      dim3 grid(unsigned((row1 - row0 + 256 * kPermRows - 1) / (256 * kPermRows)), unsigned((pr + cpb - 1) / cpb));
       permute_rows_in<<<grid, 256, 0, st>>>(d_w + size_t(pc0) * ldw, ldw, H->d_prow.as<int32_t>(), row0, row1, pr,
                                             cpb, H->d_wp.as<double>() + 16 * size_t(pc0), int64_t(H->ws_r) * 16);
     }
@@ -2787,7 +2804,7 @@ int gofmm_exact_rows(gofmm_handle* H, const int32_t* rows, int32_t nrows, const 
     encode_maps(H, r);
     {
       const int cpb = int(std::max<int64_t>(1, std::min<int64_t>(8, (48ll << 20) / (int64_t(H->n) * 8))));
-      dim3 grid(unsigned((H->ld_wp + 255) / 256), unsigned((r + cpb - 1) / cpb));
+      dim3 grid(unsigned((H->ld_wp + 256 * kPermRows - 1) / (256 * kPermRows)), unsigned((r + cpb - 1) / cpb));
       permute_rows_in<<<grid, 256, 0, st>>>(d_w, ldw, H->d_prow.as<int32_t>(), 0, H->ld_wp, r, cpb,
                                             H->d_wp.as<double>(), int64_t(H->ws_r) * 16);
     }

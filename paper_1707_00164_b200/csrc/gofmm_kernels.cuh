@@ -661,16 +661,32 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
 // wp[t, c] = w[prow[t], c]   (evaluate.hpp:294-295) into the padded leaf layout, stored in
 // 16-row panels (panel stride `pstride` doubles); prow = -1 marks padding rows (written as 0).
 // Rows [row0, row1) only (a rank's own leaves in a distributed evaluation).
+// Each thread gathers kPermRows rows (stride blockDim) of every column it visits, all loads of a
+// column issued before their stores: the random 8-byte gathers are latency-bound, so the ILP (and
+// 8x fewer blocks than one row per thread) is what moves them.
+constexpr int kPermRows = 8;
 static __global__ void permute_rows_in(const double* __restrict__ w, int64_t ldw, const int32_t* __restrict__ prow,
                                 int64_t row0, int64_t row1, int32_t r, int32_t cols_per_block,
                                 double* __restrict__ wp, int64_t pstride) {
-  const int64_t t = row0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= row1) return;
-  const int32_t src = prow[t];
+  const int64_t tb = row0 + int64_t(blockIdx.x) * blockDim.x * kPermRows + threadIdx.x;
+  int32_t src[kPermRows];
+#pragma unroll
+  for (int i = 0; i < kPermRows; ++i) {
+    const int64_t t = tb + int64_t(i) * blockDim.x;
+    src[i] = t < row1 ? prow[t] : -2;
+  }
   const int c0 = blockIdx.y * cols_per_block;
   const int c1 = min(r, c0 + cols_per_block);
-  double* dst = wp + (t >> 4) * pstride + (t & 15);
-  for (int c = c0; c < c1; ++c) dst[size_t(c) * 16] = (src >= 0) ? __ldg(w + src + size_t(c) * ldw) : 0.0;
+  for (int c = c0; c < c1; ++c) {
+    double v[kPermRows];
+#pragma unroll
+    for (int i = 0; i < kPermRows; ++i) v[i] = (src[i] >= 0) ? __ldg(w + src[i] + size_t(c) * ldw) : 0.0;
+#pragma unroll
+    for (int i = 0; i < kPermRows; ++i) {
+      const int64_t t = tb + int64_t(i) * blockDim.x;
+      if (src[i] != -2) wp[(t >> 4) * pstride + (t & 15) + size_t(c) * 16] = v[i];
+    }
+  }
 }
 
 // Distributed evaluation: copy whole 16-row panels (first r columns) between the workspace
