@@ -614,7 +614,12 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
     const int flags = cur.flags;
     Pos nxt = cur;
     advance(nxt);
-    if (s + 1 < total) stage_in(s + 1, nxt);
+    // generated operands: the next stage's tile is generated in the MIDDLE of this stage's DMMAs
+    // (after k-step kGenAfter), so the warp's own queued DMMAs keep the FP64 pipe busy through
+    // the generation's dependent-latency chains (all warps of an SM sub-partition reach that
+    // point together; generating before the stage's first DMMA left the pipe idle meanwhile)
+    constexpr int kGenAfter = kGen ? 2 : kBK / 4;
+    if (!kGen && s + 1 < total) stage_in(s + 1, nxt);
     mbar_wait(smem_u32(&bars[stage]), (s / STAGES) & 1);
     if constexpr (kGen) mbar_wait(smem_u32(&bars[2 * STAGES + stage]), (s / STAGES) & 1);
     const bool rowA = (flags & (kTermRowMajorA | kTermGen)) != 0;  // generated tiles are row-major
@@ -622,6 +627,7 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
     const uint32_t tB = sB_u + stage * S::B_STAGE_BYTES;
 #pragma unroll
     for (int ks = 0; ks < kBK / 4; ++ks) {
+      if (kGen && ks == kGenAfter && s + 1 < total) stage_in(s + 1, nxt);
       double a[S::MT];
 #pragma unroll
       for (int i = 0; i < S::MT; ++i) {
