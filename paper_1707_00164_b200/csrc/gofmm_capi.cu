@@ -291,6 +291,7 @@ struct Launch {
   int first_group = 0, ngroups = 0;      // groups [first_group, first_group + ngroups)
   int reduce_first = 0, reduce_n = 0;    // split-chain reductions after this launch (chain_reduce)
   int first_tile32 = 0, ntiles32 = 0;    // FP32 plan: 128-row tiles of the same groups
+  int64_t chain_sum32 = 0, chain_max32 = 0;  // k-stages over / longest chain of its FP32 tiles
   // output launch of a host-buffer evaluation: split into row-contiguous parts so the D2H of a
   // part's u rows overlaps the next part's kernel. parts[p] = first tile of part p in each tile
   // list and the u_perm rows it completes; parts.back() is the end sentinel. Empty = no split.
@@ -602,9 +603,10 @@ struct gofmm_handle {
   int32_t ws32_r = 0;
   bool plan32_uploaded = false;
   gofmm::f32::KernelParams kp32{};
-  gofmm::f32::GemmKernel k32_s, k32_g;  // stored-only / generated launches for the current bn
-  gofmm::f32::BMaps maps32{};
-  int32_t maps32_r = 0;
+  // FP32 kernels and B maps per N tile (index 0/1/2 = 64/128/256 columns); each launch picks its own
+  gofmm::f32::GemmKernel k32_s[3], k32_g[3];
+  gofmm::f32::BMaps maps32[3]{};
+  int32_t maps32_rv[3] = {0, 0, 0};
 
   gofmm::KernelFn kfn_sw = nullptr, kfn_sg = nullptr;
   size_t smem_sw = 0, smem_sg = 0;
@@ -742,6 +744,13 @@ void build_f32(gofmm_handle* H) {
     for (int gi = L.first_group; gi < L.first_group + L.ngroups; ++gi)
       for (int m0 = 0; m0 < std::max(H->groups[gi].M, 0); m0 += f32::kBM) tiles32.push_back({gi, m0});
     L.ntiles32 = int(tiles32.size()) - L.first_tile32;
+    L.chain_sum32 = L.chain_max32 = 0;
+    for (int i = L.first_tile32; i < L.first_tile32 + L.ntiles32; ++i) {
+      int64_t w = 0;
+      for (const HostTerm& t : H->groups[tiles32[i].group].terms) w += (t.K + 15) / 16;
+      L.chain_sum32 += w;
+      L.chain_max32 = std::max(L.chain_max32, w);
+    }
     for (size_t p = 0; p < L.parts.size(); ++p) {
       const int gb = (p + 1 < L.parts.size()) ? L.first_group + int(int64_t(L.ngroups) * p / kOutParts)
                                                : L.first_group + L.ngroups;
@@ -1870,7 +1879,7 @@ void ensure_workspace32(gofmm_handle* H, int32_t r) {
     H->d_c32[p].alloc(size_t(H->ld_s) * r * sizeof(float));
   }
   H->ws32_r = r;
-  H->maps32_r = 0;
+  for (auto& v : H->maps32_rv) v = 0;
 }
 
 // B operand view of an FP32 panel buffer: {16 rows-in-panel, r columns, rows/16 panels}, boxes
@@ -1888,22 +1897,35 @@ void encode_bmap32(CUtensorMap* map, const float* ptr, int64_t rows, int32_t r, 
 
 // FP32 kernels for this column count (N tile) and the B tensor maps over the workspace
 void prepare32(gofmm_handle* H, int32_t r) {
-  const int bn = f32_bn(r);
-  if (H->k32_s.bn != bn) {
-    H->k32_s = f32::pick_gemm(kKindNone, 1, bn);
-    if (H->kfn_g) H->k32_g = f32::pick_gemm(H->kernel, H->dim, bn);
-    GOFMM_CUDA(cudaGetLastError());
-    H->maps32_r = 0;
+  const float* bufs[3][2] = {{H->d_wp32[0].as<float>(), H->d_wp32[1].as<float>()},
+                             {H->d_what32[0].as<float>(), H->d_what32[1].as<float>()},
+                             {H->d_c32[0].as<float>(), H->d_c32[1].as<float>()}};
+  const int64_t rows[3] = {H->ld_wp, H->ld_s, H->ld_s};
+  for (int v = 0; v < 3; ++v) {
+    const int bn = 64 << v;
+    if (bn > f32_bn(r)) break;  // N tiles wider than the chunk's columns are never picked
+    if (!H->k32_s[v].fn) {
+      H->k32_s[v] = f32::pick_gemm(kKindNone, 1, bn);
+      if (H->kfn_g) H->k32_g[v] = f32::pick_gemm(H->kernel, H->dim, bn);
+      GOFMM_CUDA(cudaGetLastError());
+    }
+    if (H->maps32_rv[v] != r) {
+      for (int b = 0; b < 3; ++b)
+        for (int p = 0; p < 2; ++p) encode_bmap32(&H->maps32[v].m[b][p], bufs[b][p], rows[b], r, H->ws32_r, bn);
+      H->maps32_rv[v] = r;
+    }
   }
-  if (H->maps32_r != r) {
-    const float* bufs[3][2] = {{H->d_wp32[0].as<float>(), H->d_wp32[1].as<float>()},
-                               {H->d_what32[0].as<float>(), H->d_what32[1].as<float>()},
-                               {H->d_c32[0].as<float>(), H->d_c32[1].as<float>()}};
-    const int64_t rows[3] = {H->ld_wp, H->ld_s, H->ld_s};
-    for (int b = 0; b < 3; ++b)
-      for (int p = 0; p < 2; ++p) encode_bmap32(&H->maps32.m[b][p], bufs[b][p], rows[b], r, H->ws32_r, bn);
-    H->maps32_r = r;
-  }
+}
+
+// N tile of one FP32 launch: the widest tile that fits the chunk is the most efficient per flop;
+// a launch whose tiles leave most SMs idle (the upper tree levels: 2-64 tiles) halves its N tile
+// while the doubled CTA count still fits on the SMs — each CTA's chain runs on fewer columns.
+// (Narrowing a launch that already fills the SMs was measured slower: c2 downward levels 7-8.)
+int pick_bn32(const gofmm_handle* H, const Launch& L, int32_t r) {
+  int v = 0;
+  while (v < 2 && (64 << (v + 1)) <= f32_bn(r)) ++v;
+  while (v > 0 && int64_t(L.ntiles32) * ((r + (64 << (v - 1)) - 1) / (64 << (v - 1))) <= H->num_sms) --v;
+  return v;
 }
 
 // stage 0: the whole evaluation; stage 1 / 2: the distributed halves around the all-gather
@@ -1939,21 +1961,22 @@ void enqueue_chunk32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, 
     }
     const size_t li = size_t(&L - H->launches.data());
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li], st));
-    const f32::GemmKernel& k = L.gen ? H->k32_g : H->k32_s;
+    const int v = pick_bn32(H, L, r);
+    const f32::GemmKernel& k = L.gen ? H->k32_g[v] : H->k32_s[v];
     if (rows_done && stage == 0 && L.out == Buf::Out && !L.parts.empty() && L.ntiles32 >= 8 * H->num_sms) {
       for (size_t p = 0; p + 1 < L.parts.size(); ++p) {
         const int t0 = L.parts[p].tile32, nt = L.parts[p + 1].tile32 - t0;
         if (nt > 0)
-          GOFMM_CUDA(f32::launch_gemm(k, unsigned(nt), r, H->maps32, H->d_tiles32.as<Tile>() + t0,
+          GOFMM_CUDA(f32::launch_gemm(k, unsigned(nt), r, H->maps32[v], H->d_tiles32.as<Tile>() + t0,
                                       H->d_groups.as<Group>(), H->d_terms32.as<f32::Term>(), H->kp32, ch, cl, ldc,
-                                      cpanel, st));
+                                      cpanel, st, H->pdl));
         (*rows_done)(L.parts[p].row, L.parts[p + 1].row);
       }
       if (rows_used) *rows_used = true;
     } else {
-      GOFMM_CUDA(f32::launch_gemm(k, unsigned(L.ntiles32), r, H->maps32, H->d_tiles32.as<Tile>() + L.first_tile32,
+      GOFMM_CUDA(f32::launch_gemm(k, unsigned(L.ntiles32), r, H->maps32[v], H->d_tiles32.as<Tile>() + L.first_tile32,
                                   H->d_groups.as<Group>(), H->d_terms32.as<f32::Term>(), H->kp32, ch, cl, ldc, cpanel,
-                                  st));
+                                  st, H->pdl));
     }
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li + 1], st));
   }
@@ -2469,9 +2492,10 @@ int gofmm_launch_profile(const gofmm_handle* H, int32_t r, int32_t cap, gofmm_la
       const Launch& L = H->launches[i];
       out[i].phase = L.phase;
       out[i].level = L.level;
-      if (H->precision == GOFMM_PRECISION_F32)
-        out[i].ctas = int64_t(L.ntiles32) * ((r + f32_bn(r) - 1) / f32_bn(r));
-      else {
+      if (H->precision == GOFMM_PRECISION_F32) {
+        const int bn = 64 << pick_bn32(H, L, r);
+        out[i].ctas = int64_t(L.ntiles32) * ((r + bn - 1) / bn);
+      } else {
         const LaunchCfg cfg = pick_launch_cfg(H, L, r);
         out[i].ctas = int64_t(L.tn[cfg.bm_class]) * ((r + cfg.bn - 1) / cfg.bn);
       }

@@ -160,10 +160,18 @@ GemmKernel pick_gemm(int kind, int dim, int bn) {
 
 cudaError_t launch_gemm(const GemmKernel& k, unsigned ntiles, int32_t R, const BMaps& maps, const Tile* tiles,
                         const Group* groups, const Term* terms, const KernelParams& kp, float* c_hi, float* c_lo,
-                        int64_t ldc, int32_t cpanel, cudaStream_t st) {
-  dim3 grid(ntiles, unsigned((R + k.bn - 1) / k.bn));
-  k.fn<<<grid, kThreads, k.smem, st>>>(maps, tiles, groups, terms, R, kp, c_hi, c_lo, ldc, cpanel);
-  return cudaGetLastError();
+                        int64_t ldc, int32_t cpanel, cudaStream_t st, bool pdl) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ntiles, unsigned((R + k.bn - 1) / k.bn));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = k.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k.fn, maps, tiles, groups, terms, R, kp, c_hi, c_lo, ldc, cpanel);
 }
 
 cudaError_t launch_permute_in(const float* w, int64_t ldw, const int32_t* prow, int64_t row0, int64_t row1, int32_t r,

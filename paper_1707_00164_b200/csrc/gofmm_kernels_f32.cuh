@@ -265,6 +265,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+  // programmatic dependent launch (host: launch_gemm): prologue done, the B / C buffers are written
+  // by earlier launches
+  pdl_launch_dependents();
+  pdl_wait();
 
   int total = 0;
   for (int t = grp.tbeg; t < grp.tend; ++t) total += (terms[t].K + kBK - 1) / kBK;
@@ -579,7 +583,7 @@ struct GemmKernel {
 GemmKernel pick_gemm(int kind, int dim, int bn);
 cudaError_t launch_gemm(const GemmKernel& k, unsigned ntiles, int32_t R, const BMaps& maps, const Tile* tiles,
                         const Group* groups, const Term* terms, const KernelParams& kp, float* c_hi, float* c_lo,
-                        int64_t ldc, int32_t cpanel, cudaStream_t st);
+                        int64_t ldc, int32_t cpanel, cudaStream_t st, bool pdl = false);
 cudaError_t launch_permute_in(const float* w, int64_t ldw, const int32_t* prow, int64_t row0, int64_t row1, int32_t r,
                               int64_t n, float* wh, float* wl, int64_t pstride, cudaStream_t st);
 cudaError_t launch_unpermute(const float* up, int64_t ldp, const int32_t* iperm, int64_t n, int32_t r, float* u,
