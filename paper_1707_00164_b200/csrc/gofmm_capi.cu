@@ -711,7 +711,10 @@ void build_f32(gofmm_handle* H) {
     GOFMM_CUDA(cudaStreamSynchronize(H->stream));
   }
   if (H->source == GOFMM_SOURCE_KERNEL) {
-    const int64_t nxp = int64_t(H->ld_wp) * H->dim, nxs = int64_t(H->ld_s) * H->dim;
+    // skeleton-space coordinates exist for the node rows only (split-chain scratch rows extend
+    // ld_s after d_xs was sized and carry no points)
+    const int64_t xs_rows = int64_t(H->d_xs.bytes / sizeof(double)) / std::max(H->dim, 1);
+    const int64_t nxp = int64_t(H->ld_wp) * H->dim, nxs = xs_rows * H->dim;
     H->d_xp32.alloc(size_t(nxp) * sizeof(float), false);
     H->d_xs32.alloc(size_t(std::max<int64_t>(nxs, 1)) * sizeof(float), false);
     GOFMM_CUDA(f32::launch_to_f32(H->d_xp.as<double>(), nxp, H->d_xp32.as<float>(), H->stream));
@@ -723,7 +726,7 @@ void build_f32(gofmm_handle* H) {
       H->d_xsn32.alloc(size_t(std::max<int64_t>(H->ld_s, 16)) * sizeof(float));
       GOFMM_CUDA(f32::launch_scaled_norms(H->d_xp.as<double>(), H->ld_wp, H->dim, sc, H->d_xpn32.as<float>(), H->stream));
       if (H->d_xs.p)
-        GOFMM_CUDA(f32::launch_scaled_norms(H->d_xs.as<double>(), H->ld_s, H->dim, sc, H->d_xsn32.as<float>(), H->stream));
+        GOFMM_CUDA(f32::launch_scaled_norms(H->d_xs.as<double>(), xs_rows, H->dim, sc, H->d_xsn32.as<float>(), H->stream));
     }
     GOFMM_CUDA(cudaStreamSynchronize(H->stream));
   }
@@ -1244,13 +1247,13 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     // Latency-bound levels (few groups, long far-field chains — the upper levels; config 1 has
     // chains of 80 k-stages on 16-64 groups): split a chain that is much longer than the level's
     // per-SM share into segments of about that share. Segment 0 accumulates into the group's own
-    // rows, the others into scratch rows appended to skeleton space; chain_reduce adds them in
-    // segment order after the launch. FP64 only (the FP32 epilogue stores hi/lo operands).
+    // rows, the others into scratch rows appended to skeleton space; chain_reduce (FP32:
+    // chain_reduce_f32 over the hi / lo pair) adds them in segment order after the launch.
     // The split (and so the summation order of c) is a function of the WHOLE level and a fixed SM
     // count only — never of this device's SM count or of a rank's share of the level — so u is
     // bitwise the same on any GPU SKU and for every rank layout of the subtree split.
     const int first_reduce = int(H->reduces.size());
-    if (H->precision == GOFMM_PRECISION_F64 && !gs.empty()) {
+    if (!gs.empty()) {
       auto stages = [](const HostTerm& t) { return int64_t((t.K + 15) / 16); };
       auto kstages = [](int64_t k) { return (k + 15) / 16; };
       int64_t sum = 0, mx = 0;
@@ -1978,6 +1981,9 @@ void enqueue_chunk32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, 
                                   H->d_groups.as<Group>(), H->d_terms32.as<f32::Term>(), H->kp32, ch, cl, ldc, cpanel,
                                   st, H->pdl));
     }
+    if (L.reduce_n > 0)  // split term chains: segments 1.. into the group rows
+      GOFMM_CUDA(f32::launch_chain_reduce(H->d_reduces.as<ChainReduce>() + L.reduce_first, L.reduce_n,
+                                          H->d_reduce_src.as<int64_t>(), ch, cl, ldc, r, st, H->pdl));
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li + 1], st));
   }
   if (stage == 1 && H->n_pack > 0)

@@ -42,6 +42,31 @@ static __global__ void permute_rows_in_f32(const float* __restrict__ w, int64_t 
   }
 }
 
+// Split term chains (see chain_reduce in gofmm_kernels.cuh): segment partials in scratch rows of
+// the hi / lo panel pair are added to the group's rows in segment order; each partial is the FP32
+// accumulator the epilogue split as hi + lo, so the sum is formed from hi + lo and split again.
+static __global__ void chain_reduce_f32(const ChainReduce* __restrict__ items, const int64_t* __restrict__ src_rows,
+                                        float* __restrict__ ch, float* __restrict__ cl, int64_t pstride, int32_t r) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const ChainReduce it = items[blockIdx.x];
+  const int64_t total = int64_t(it.M) * r;
+  for (int64_t e = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.y) * blockDim.x) {
+    const int m = int(e % it.M), n = int(e / it.M);
+    auto off = [&](int64_t row) { return (row >> 4) * pstride + 16 * int64_t(n) + (row & 15); };
+    const int64_t d = off(it.dst_row + m);
+    float acc = ch[d] + cl[d];
+    for (int q = 0; q < it.nsrc; ++q) {
+      const int64_t o = off(src_rows[it.src_first + q] + m);
+      acc += ch[o] + cl[o];
+    }
+    float hi, lo;
+    split_tf32(acc, hi, lo);
+    ch[d] = hi;
+    cl[d] = lo;
+  }
+}
+
 // u[iperm[t], c] = up[t, c]
 static __global__ void unpermute_rows_f32(const float* __restrict__ up, int64_t ldp, const int32_t* __restrict__ iperm,
                                    int64_t n, int32_t r, int32_t cols_per_block, float* __restrict__ u, int64_t ldu) {
@@ -172,6 +197,21 @@ cudaError_t launch_gemm(const GemmKernel& k, unsigned ntiles, int32_t R, const B
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k.fn, maps, tiles, groups, terms, R, kp, c_hi, c_lo, ldc, cpanel);
+}
+
+cudaError_t launch_chain_reduce(const ChainReduce* items, int n, const int64_t* src_rows, float* ch, float* cl,
+                                int64_t pstride, int32_t r, cudaStream_t st, bool pdl) {
+  if (n <= 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(n), 8);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, chain_reduce_f32, items, src_rows, ch, cl, pstride, r);
 }
 
 cudaError_t launch_permute_in(const float* w, int64_t ldw, const int32_t* prow, int64_t row0, int64_t row1, int32_t r,

@@ -584,6 +584,8 @@ GemmKernel pick_gemm(int kind, int dim, int bn);
 cudaError_t launch_gemm(const GemmKernel& k, unsigned ntiles, int32_t R, const BMaps& maps, const Tile* tiles,
                         const Group* groups, const Term* terms, const KernelParams& kp, float* c_hi, float* c_lo,
                         int64_t ldc, int32_t cpanel, cudaStream_t st, bool pdl = false);
+cudaError_t launch_chain_reduce(const ChainReduce* items, int n, const int64_t* src_rows, float* ch, float* cl,
+                                int64_t pstride, int32_t r, cudaStream_t st, bool pdl);
 cudaError_t launch_permute_in(const float* w, int64_t ldw, const int32_t* prow, int64_t row0, int64_t row1, int32_t r,
                               int64_t n, float* wh, float* wl, int64_t pstride, cudaStream_t st);
 cudaError_t launch_unpermute(const float* up, int64_t ldp, const int32_t* iperm, int64_t n, int32_t r, float* u,
