@@ -531,7 +531,10 @@ struct gofmm_handle {
   cudaGraphExec_t gexec = nullptr;
   std::tuple<const void*, int64_t, const void*, int64_t, int32_t, int32_t, int32_t> gkey{};
   bool graphs = true;  // GOFMM_NO_GRAPH=1 disables replay
-  bool pdl = true;     // programmatic dependent launch between level launches (GOFMM_NO_PDL=1 disables)
+  // programmatic dependent launch between level launches (GOFMM_NO_PDL=1 disables); never in timed
+  // (event-instrumented) enqueues: an event between two launches breaks the programmatic edge, and
+  // the host pipeline measured slower and jittery with it (N = 2^16: 37-47 vs 34 ms per call)
+  bool pdl = true;
   cudaEvent_t pev[2][4] = {};
   cudaEvent_t tev[2][4] = {};
   cudaEvent_t dpev[8][2] = {};  // per-part D2H timing of a split output launch (<= kOutParts)
@@ -1715,9 +1718,11 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
     const int64_t row0 = 0, row1 = H->ld_wp;
     const int32_t pc0 = piece ? c0 : 0, pr = piece ? c1 - c0 : r;  // columns of this piece
     if (row1 > row0 && pr > 0) {
-      dim3 grid(unsigned((row1 - row0 + 256 * kPermRows - 1) / (256 * kPermRows)), unsigned((pr + cpb - 1) / cpb));
-      permute_rows_in<<<grid, 256, 0, st>>>(d_w + size_t(pc0) * ldw, ldw, H->d_prow.as<int32_t>(), row0, row1, pr,
-                                            cpb, H->d_wp.as<double>() + 16 * size_t(pc0), int64_t(H->ws_r) * 16);
+      const int rpt = perm_rows_per_thread(row1 - row0, pr);
+      dim3 grid(unsigned((row1 - row0 + 256 * rpt - 1) / (256 * rpt)), unsigned((pr + cpb - 1) / cpb));
+      auto* kern = rpt == kPermRows ? &permute_rows_in<kPermRows> : &permute_rows_in<1>;
+      kern<<<grid, 256, 0, st>>>(d_w + size_t(pc0) * ldw, ldw, H->d_prow.as<int32_t>(), row0, row1, pr, cpb,
+                                 H->d_wp.as<double>() + 16 * size_t(pc0), int64_t(H->ws_r) * 16);
     }
   }
   // ev[1 + p] marks the start of phase p (0 upward, 1 downward, 2 output); ev[4] the end
@@ -1750,7 +1755,7 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
     auto run = [&](int t0, int nt) {
       if (nt <= 0 || ncols <= 0) return;
       dim3 grid(unsigned(nt), unsigned((ncols + cfg.bn - 1) / cfg.bn));
-      launch_k(H->pdl, cfg.fn, grid, dim3(kThreadsG), cfg.smem, st, *cfg.maps, H->d_tiles.as<Tile>() + t0,
+      launch_k(H->pdl && !timed, cfg.fn, grid, dim3(kThreadsG), cfg.smem, st, *cfg.maps, H->d_tiles.as<Tile>() + t0,
                H->d_groups.as<Group>(), H->d_terms.as<Term>(), r, H->kp, cbase, ldc, cpanel, n_off);
     };
     // split only launches of many waves: on small trees the extra launches cost more than the
@@ -1767,7 +1772,7 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
     }
     if (L.reduce_n > 0 && !piece) {  // split term chains: segments 1.. into the group rows
       dim3 grid(unsigned(L.reduce_n), 8);
-      launch_k(H->pdl, chain_reduce, grid, dim3(256), 0, st, H->d_reduces.as<ChainReduce>() + L.reduce_first,
+      launch_k(H->pdl && !timed, chain_reduce, grid, dim3(256), 0, st, H->d_reduces.as<ChainReduce>() + L.reduce_first,
                H->d_reduce_src.as<int64_t>(), cbase, ldc, r);
     }
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li + 1], st));
@@ -1972,18 +1977,18 @@ void enqueue_chunk32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, 
         if (nt > 0)
           GOFMM_CUDA(f32::launch_gemm(k, unsigned(nt), r, H->maps32[v], H->d_tiles32.as<Tile>() + t0,
                                       H->d_groups.as<Group>(), H->d_terms32.as<f32::Term>(), H->kp32, ch, cl, ldc,
-                                      cpanel, st, H->pdl));
+                                      cpanel, st, H->pdl && !timed));
         (*rows_done)(L.parts[p].row, L.parts[p + 1].row);
       }
       if (rows_used) *rows_used = true;
     } else {
       GOFMM_CUDA(f32::launch_gemm(k, unsigned(L.ntiles32), r, H->maps32[v], H->d_tiles32.as<Tile>() + L.first_tile32,
                                   H->d_groups.as<Group>(), H->d_terms32.as<f32::Term>(), H->kp32, ch, cl, ldc, cpanel,
-                                  st, H->pdl));
+                                  st, H->pdl && !timed));
     }
     if (L.reduce_n > 0)  // split term chains: segments 1.. into the group rows
       GOFMM_CUDA(f32::launch_chain_reduce(H->d_reduces.as<ChainReduce>() + L.reduce_first, L.reduce_n,
-                                          H->d_reduce_src.as<int64_t>(), ch, cl, ldc, r, st, H->pdl));
+                                          H->d_reduce_src.as<int64_t>(), ch, cl, ldc, r, st, H->pdl && !timed));
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li + 1], st));
   }
   if (stage == 1 && H->n_pack > 0)
@@ -2629,8 +2634,11 @@ void evaluate_host(gofmm_handle* H, const T* w, int64_t ldw, int32_t r, T* u_per
   };
   // FP64 single chunk: W lands in column pieces and each piece's permutation + upward (N2S,
   // column-separable) starts as soon as it is in HBM, so the upload overlaps the upward pass
+  // (only for uploads of >= 1 GB: on small trees the pieces' repeated level launches cost more than
+  // the upload they hide — N = 2^16, r = 512: upward 14 ms in pieces vs ~1 ms in one pass)
   constexpr int32_t kPieceCols = 128;
-  const int npieces = (!kF32 && nchunks == 1 && rc > kPieceCols) ? int((rc + kPieceCols - 1) / kPieceCols) : 0;
+  const bool big = double(H->n) * double(rc) * sizeof(T) >= double(1 << 30);
+  const int npieces = (!kF32 && nchunks == 1 && rc > kPieceCols && big) ? int((rc + kPieceCols - 1) / kPieceCols) : 0;
   if (npieces > 8) throw Error(GOFMM_ERR_CUDA, "internal: too many column pieces");
   if (npieces > 0) {
     if (stats) GOFMM_CUDA(cudaEventRecord(H->tev[0][0], H->s_h2d));
@@ -2834,8 +2842,10 @@ int gofmm_exact_rows(gofmm_handle* H, const int32_t* rows, int32_t nrows, const 
     encode_maps(H, r);
     {
       const int cpb = int(std::max<int64_t>(1, std::min<int64_t>(8, (48ll << 20) / (int64_t(H->n) * 8))));
-      dim3 grid(unsigned((H->ld_wp + 256 * kPermRows - 1) / (256 * kPermRows)), unsigned((r + cpb - 1) / cpb));
-      permute_rows_in<<<grid, 256, 0, st>>>(d_w, ldw, H->d_prow.as<int32_t>(), 0, H->ld_wp, r, cpb,
+      const int rpt = perm_rows_per_thread(H->ld_wp, r);
+      dim3 grid(unsigned((H->ld_wp + 256 * rpt - 1) / (256 * rpt)), unsigned((r + cpb - 1) / cpb));
+      auto* kern = rpt == kPermRows ? &permute_rows_in<kPermRows> : &permute_rows_in<1>;
+      kern<<<grid, 256, 0, st>>>(d_w, ldw, H->d_prow.as<int32_t>(), 0, H->ld_wp, r, cpb,
                                             H->d_wp.as<double>(), int64_t(H->ws_r) * 16);
     }
     const int nleaf = int(H->leaf_ids.size());

@@ -13,24 +13,25 @@ namespace {
 // wp_{hi,lo}[t, c] = split(w[prow[t], c]) in 16-row panels (evaluate.hpp:294-295)
 // kPermRows rows per thread (stride blockDim), all loads of a column before their stores (ILP for
 // the latency-bound random gathers, as in the FP64 permute_rows_in)
-static __global__ void permute_rows_in_f32(const float* __restrict__ w, int64_t ldw, const int32_t* __restrict__ prow,
+template <int RPT>
+__global__ void permute_rows_in_f32(const float* __restrict__ w, int64_t ldw, const int32_t* __restrict__ prow,
                                     int64_t row0, int64_t row1, int32_t r, int32_t cols_per_block,
                                     float* __restrict__ wh, float* __restrict__ wl, int64_t pstride) {
-  const int64_t tb = row0 + int64_t(blockIdx.x) * blockDim.x * kPermRows + threadIdx.x;
-  int32_t src[kPermRows];
+  const int64_t tb = row0 + int64_t(blockIdx.x) * blockDim.x * RPT + threadIdx.x;
+  int32_t src[RPT];
 #pragma unroll
-  for (int i = 0; i < kPermRows; ++i) {
+  for (int i = 0; i < RPT; ++i) {
     const int64_t t = tb + int64_t(i) * blockDim.x;
     src[i] = t < row1 ? prow[t] : -2;
   }
   const int c0 = blockIdx.y * cols_per_block;
   const int c1 = min(r, c0 + cols_per_block);
   for (int c = c0; c < c1; ++c) {
-    float x[kPermRows];
+    float x[RPT];
 #pragma unroll
-    for (int i = 0; i < kPermRows; ++i) x[i] = (src[i] >= 0) ? __ldg(w + src[i] + size_t(c) * ldw) : 0.f;
+    for (int i = 0; i < RPT; ++i) x[i] = (src[i] >= 0) ? __ldg(w + src[i] + size_t(c) * ldw) : 0.f;
 #pragma unroll
-    for (int i = 0; i < kPermRows; ++i) {
+    for (int i = 0; i < RPT; ++i) {
       if (src[i] == -2) continue;
       const int64_t t = tb + int64_t(i) * blockDim.x;
       const int64_t o = (t >> 4) * pstride + (t & 15) + size_t(c) * 16;
@@ -220,8 +221,10 @@ cudaError_t launch_permute_in(const float* w, int64_t ldw, const int32_t* prow, 
   // blocks walk all rows of cpb columns before the next ones: the randomly gathered source
   // columns stay L2-resident (see the FP64 permutation in gofmm_capi.cu)
   const int cpb = int(std::max<int64_t>(1, std::min<int64_t>(8, (48ll << 20) / (std::max<int64_t>(n, 1) * 4))));
-  dim3 grid(unsigned((row1 - row0 + 256 * kPermRows - 1) / (256 * kPermRows)), unsigned((r + cpb - 1) / cpb));
-  permute_rows_in_f32<<<grid, 256, 0, st>>>(w, ldw, prow, row0, row1, r, cpb, wh, wl, pstride);
+  const int rpt = perm_rows_per_thread(row1 - row0, r);
+  dim3 grid(unsigned((row1 - row0 + 256 * rpt - 1) / (256 * rpt)), unsigned((r + cpb - 1) / cpb));
+  auto* kern = rpt == kPermRows ? &permute_rows_in_f32<kPermRows> : &permute_rows_in_f32<1>;
+  kern<<<grid, 256, 0, st>>>(w, ldw, prow, row0, row1, r, cpb, wh, wl, pstride);
   return cudaGetLastError();
 }
 

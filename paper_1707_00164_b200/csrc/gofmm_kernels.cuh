@@ -667,28 +667,31 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
 // wp[t, c] = w[prow[t], c]   (evaluate.hpp:294-295) into the padded leaf layout, stored in
 // 16-row panels (panel stride `pstride` doubles); prow = -1 marks padding rows (written as 0).
 // Rows [row0, row1) only (a rank's own leaves in a distributed evaluation).
-// Each thread gathers kPermRows rows (stride blockDim) of every column it visits, all loads of a
-// column issued before their stores: the random 8-byte gathers are latency-bound, so the ILP (and
-// 8x fewer blocks than one row per thread) is what moves them.
+// Each thread gathers RPT rows (stride blockDim) of every column it visits, all loads of a column
+// issued before their stores: the random 8-byte gathers are latency-bound, so on large W the ILP
+// (and RPT x fewer blocks) is what moves them (RPT = kPermRows); small W keeps one row per thread
+// for parallelism (perm_rows_per_thread).
 constexpr int kPermRows = 8;
-static __global__ void permute_rows_in(const double* __restrict__ w, int64_t ldw, const int32_t* __restrict__ prow,
+inline int perm_rows_per_thread(int64_t rows, int32_t r) { return double(rows) * r >= 6.4e7 ? kPermRows : 1; }
+template <int RPT>
+__global__ void permute_rows_in(const double* __restrict__ w, int64_t ldw, const int32_t* __restrict__ prow,
                                 int64_t row0, int64_t row1, int32_t r, int32_t cols_per_block,
                                 double* __restrict__ wp, int64_t pstride) {
-  const int64_t tb = row0 + int64_t(blockIdx.x) * blockDim.x * kPermRows + threadIdx.x;
-  int32_t src[kPermRows];
+  const int64_t tb = row0 + int64_t(blockIdx.x) * blockDim.x * RPT + threadIdx.x;
+  int32_t src[RPT];
 #pragma unroll
-  for (int i = 0; i < kPermRows; ++i) {
+  for (int i = 0; i < RPT; ++i) {
     const int64_t t = tb + int64_t(i) * blockDim.x;
     src[i] = t < row1 ? prow[t] : -2;
   }
   const int c0 = blockIdx.y * cols_per_block;
   const int c1 = min(r, c0 + cols_per_block);
   for (int c = c0; c < c1; ++c) {
-    double v[kPermRows];
+    double v[RPT];
 #pragma unroll
-    for (int i = 0; i < kPermRows; ++i) v[i] = (src[i] >= 0) ? __ldg(w + src[i] + size_t(c) * ldw) : 0.0;
+    for (int i = 0; i < RPT; ++i) v[i] = (src[i] >= 0) ? __ldg(w + src[i] + size_t(c) * ldw) : 0.0;
 #pragma unroll
-    for (int i = 0; i < kPermRows; ++i) {
+    for (int i = 0; i < RPT; ++i) {
       const int64_t t = tb + int64_t(i) * blockDim.x;
       if (src[i] != -2) wp[(t >> 4) * pstride + (t & 15) + size_t(c) * 16] = v[i];
     }

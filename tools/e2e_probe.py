@@ -13,7 +13,14 @@ from paper_1707_00164_b200 import Evaluator, synth  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c1"
 prec = sys.argv[2] if len(sys.argv) > 2 else "fp64"
-tree, c = synth.make_config_tree(cfg)
+n = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # > 0: the product compress of the config's cloud at n
+if n:
+    import bench
+
+    c = dict(synth.CONFIGS[cfg], name=cfg)
+    tree, _ = bench.workload_tree(c, n, 0, "compress")
+else:
+    tree, c = synth.make_config_tree(cfg)
 r = c["r"]
 dt = torch.float64 if prec == "fp64" else torch.float32
 with Evaluator(tree, precision=prec) as ev:
