@@ -24,6 +24,7 @@
 #include <cuda.h>
 
 #include <cstdint>
+#include <type_traits>
 
 namespace gofmm {
 
@@ -565,6 +566,11 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
     }
   }
 
+  // 8-row fragments of this warp that hold output rows: a group's last m-tile is partial whenever
+  // its row count (a skeleton rank) is not a multiple of BM, and the fragments wholly past M are
+  // skipped (warp-uniform) — e.g. rank 455 in 32-row tiles: the 15th tile runs 1 of 4 fragments
+  const int mfrag = min(S::MT, max(0, (M - m0 - wm0 + 7) / 8));
+
   // swizzled B fragment offsets: row n = wn0 + 8j + g has (n & 7) == g
   uint32_t boff[kBK / 4];
 #pragma unroll
@@ -625,21 +631,39 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
     const bool rowA = (flags & (kTermRowMajorA | kTermGen)) != 0;  // generated tiles are row-major
     const uint32_t tA = sA_u + stage * S::A_STAGE * 8;
     const uint32_t tB = sB_u + stage * S::B_STAGE_BYTES;
+    // one stage of DMMAs on the first MF 8-row fragments (MF = MT: every full tile; the partial
+    // last tile of a group takes the instantiation for its fragment count — a warp-uniform branch
+    // outside the unrolled loop, so full tiles keep their schedule)
+    auto mma_stage = [&](auto mf_tag) {
+      constexpr int MF = decltype(mf_tag)::value;
 #pragma unroll
-    for (int ks = 0; ks < kBK / 4; ++ks) {
-      if (kGen && ks == kGenAfter && s + 1 < total) stage_in(s + 1, nxt);
-      double a[S::MT];
+      for (int ks = 0; ks < kBK / 4; ++ks) {
+        if (kGen && ks == kGenAfter && s + 1 < total) stage_in(s + 1, nxt);
+        double a[S::MT];
 #pragma unroll
-      for (int i = 0; i < S::MT; ++i) {
-        const int kk = kpi(ks, tig), m = wm0 + 8 * i + g;
-        a[i] = lds64(tA + (rowA ? swz128(m, kk) : acm64(m, kk)));
+        for (int i = 0; i < MF; ++i) {
+          const int kk = kpi(ks, tig), m = wm0 + 8 * i + g;
+          a[i] = lds64(tA + (rowA ? swz128(m, kk) : acm64(m, kk)));
+        }
+#pragma unroll
+        for (int j = 0; j < S::NT; ++j) {
+          const double b = lds64(tB + boff[ks] + 1024u * j);
+#pragma unroll
+          for (int i = 0; i < MF; ++i) dmma884(acc[i][j][0], acc[i][j][1], a[i], b);
+        }
       }
-#pragma unroll
-      for (int j = 0; j < S::NT; ++j) {
-        const double b = lds64(tB + boff[ks] + 1024u * j);
-#pragma unroll
-        for (int i = 0; i < S::MT; ++i) dmma884(acc[i][j][0], acc[i][j][1], a[i], b);
-      }
+    };
+    if (mfrag >= S::MT) {
+      mma_stage(std::integral_constant<int, S::MT>{});
+    } else if constexpr (S::MT >= 4) {
+      if (mfrag <= S::MT / 4)
+        mma_stage(std::integral_constant<int, (S::MT >= 4 ? S::MT / 4 : 1)>{});
+      else if (mfrag <= S::MT / 2)
+        mma_stage(std::integral_constant<int, (S::MT >= 4 ? S::MT / 2 : 1)>{});
+      else
+        mma_stage(std::integral_constant<int, S::MT>{});
+    } else {
+      mma_stage(std::integral_constant<int, S::MT>{});
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&bars[STAGES + stage]));
