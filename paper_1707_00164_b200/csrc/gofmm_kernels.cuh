@@ -653,13 +653,11 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
         }
       }
     };
-    if (mfrag >= S::MT) {
-      mma_stage(std::integral_constant<int, S::MT>{});
-    } else if constexpr (S::MT >= 4) {
-      if (mfrag <= S::MT / 4)
-        mma_stage(std::integral_constant<int, (S::MT >= 4 ? S::MT / 4 : 1)>{});
-      else if (mfrag <= S::MT / 2)
-        mma_stage(std::integral_constant<int, (S::MT >= 4 ? S::MT / 2 : 1)>{});
+    // (only the 4-fragment warp tiles get a second, one-fragment copy: every extra copy of the
+    // unrolled stage costs instruction-cache footprint — a 3-copy variant slowed the G config 20 %)
+    if constexpr (S::MT >= 4) {
+      if (mfrag == 1)
+        mma_stage(std::integral_constant<int, 1>{});
       else
         mma_stage(std::integral_constant<int, S::MT>{});
     } else {
