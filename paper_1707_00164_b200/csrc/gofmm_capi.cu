@@ -559,6 +559,9 @@ struct gofmm_handle {
   // device tree
   gofmm::DevBuf d_proj, d_diag, d_near, d_far, d_xp, d_xs, d_prow, d_iperm;
   gofmm::DevBuf d_amaps;  // TMA descriptors of the stored-A terms (upload_plan)
+  gofmm::DevBuf d_perm32;  // FP32 two-pass permutation: row-major copy of W (large W only)
+  int32_t perm2 = -1;      // GOFMM_PERM2=1 / 0 forces the two-pass FP32 permutation on / off
+  bool perm2_on = false;   // the current chunk uses it (prepare32)
   std::vector<int64_t> proj_off, diag_off, near_off, far_off;  // device blob offsets (doubles)
 
   // plan
@@ -851,6 +854,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   }
   if (const char* e = std::getenv("GOFMM_NO_GRAPH")) H->graphs = !(e[0] == '1');
   if (const char* e = std::getenv("GOFMM_NO_PDL")) H->pdl = !(e[0] == '1');
+  if (const char* e = std::getenv("GOFMM_PERM2")) H->perm2 = (e[0] == '1') ? 1 : 0;
   auto cp = [&](std::vector<int32_t>& v, const int32_t* p, int64_t k) { v.assign(p, p + k); };
   cp(H->parent, d->parent, nn);
   cp(H->left, d->left, nn);
@@ -1905,6 +1909,19 @@ void encode_bmap32(CUtensorMap* map, const float* ptr, int64_t rows, int32_t r, 
 
 // FP32 kernels for this column count (N tile) and the B tensor maps over the workspace
 void prepare32(gofmm_handle* H, int32_t r) {
+  {  // two-pass permutation for W >= 4 GB (enqueue_chunk32) when its row-major scratch fits in HBM
+    const int64_t ldt = (int64_t(r) + 3) & ~int64_t(3);
+    const size_t need = size_t(H->n) * size_t(ldt) * sizeof(float);
+    H->perm2_on = H->perm2 >= 0 ? H->perm2 == 1 : double(H->n) * double(r) * sizeof(float) >= double(4ll << 30);
+    if (H->perm2_on && H->d_perm32.bytes < need) {
+      size_t free_b = 0, total_b = 0;
+      GOFMM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      if (free_b > need + (size_t(2) << 30))
+        H->d_perm32.alloc(need, false);
+      else
+        H->perm2_on = false;
+    }
+  }
   const float* bufs[3][2] = {{H->d_wp32[0].as<float>(), H->d_wp32[1].as<float>()},
                              {H->d_what32[0].as<float>(), H->d_what32[1].as<float>()},
                              {H->d_c32[0].as<float>(), H->d_c32[1].as<float>()}};
@@ -1951,7 +1968,16 @@ void enqueue_chunk32(gofmm_handle* H, const float* d_w, int64_t ldw, int32_t r, 
                                       pstride, d_xbuf, r, H->dist.max_send_rows, 0, st));
   if (stage == 0 || stage == 1) {  // every row, also in stage 1 (W is replicated, see enqueue_chunk)
     const int64_t row0 = 0, row1 = H->ld_wp;
-    GOFMM_CUDA(f32::launch_permute_in(d_w, ldw, H->d_prow.as<int32_t>(), row0, row1, r, H->n,
+    // large W (>= 4 GB): transpose + coalesced row gather (scratch sized in prepare32, before any
+    // graph capture)
+    const int64_t ldt = (int64_t(r) + 3) & ~int64_t(3);
+    const bool two_pass = H->perm2_on && H->d_perm32.bytes >= size_t(H->n) * size_t(ldt) * sizeof(float);
+    if (two_pass)
+      GOFMM_CUDA(f32::launch_permute_in_2pass(d_w, ldw, H->d_prow.as<int32_t>(), row0, row1, r, H->n,
+                                              H->d_wp32[0].as<float>(), H->d_wp32[1].as<float>(), pstride,
+                                              H->d_perm32.as<float>(), ldt, st));
+    else
+      GOFMM_CUDA(f32::launch_permute_in(d_w, ldw, H->d_prow.as<int32_t>(), row0, row1, r, H->n,
                                       H->d_wp32[0].as<float>(), H->d_wp32[1].as<float>(), pstride, st));
   }
   if (timed) GOFMM_CUDA(cudaEventRecord(H->ev[1], st));

@@ -228,6 +228,77 @@ cudaError_t launch_permute_in(const float* w, int64_t ldw, const int32_t* prow, 
   return cudaGetLastError();
 }
 
+// Two-pass permutation for large W (SURVEY.md §8d's K5 at c5 sizes): the one-pass gather above is
+// bound by L1 wavefronts of random 4-byte reads (N*r of them: 23 ms at N = 2^22, r = 1024), so W is
+// first transposed to row-major (32x32 shared-memory tiles, both sides coalesced), then every
+// destination panel gathers its 16 source rows as contiguous row segments and writes the panel
+// layout through shared memory — four coalesced streams instead of N*r random reads.
+static __global__ void __launch_bounds__(256) transpose_to_rows_f32(const float* __restrict__ w, int64_t ldw,
+                                                                     int64_t n, int32_t r, float* __restrict__ t,
+                                                                     int64_t ldt) {
+  __shared__ float tile[64][65];  // [column][row]
+  const int64_t i0 = int64_t(blockIdx.x) * 64;
+  const int c0 = blockIdx.y * 64;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  float v[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {  // column c0 + ty + 8*(q/2), rows i0 + tx + 32*(q%2): 128-byte runs
+    const int c = c0 + ty + 8 * (q >> 1);
+    const int64_t i = i0 + tx + 32 * (q & 1);
+    v[q] = (i < n && c < r) ? __ldg(w + i + size_t(c) * ldw) : 0.f;
+  }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) tile[ty + 8 * (q >> 1)][tx + 32 * (q & 1)] = v[q];
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {  // row i0 + ty + 8*(q/2), columns c0 + tx + 32*(q%2)
+    const int64_t i = i0 + ty + 8 * (q >> 1);
+    const int c = c0 + tx + 32 * (q & 1);
+    if (i < n && c < r) t[i * ldt + c] = tile[tx + 32 * (q & 1)][ty + 8 * (q >> 1)];
+  }
+}
+
+static __global__ void __launch_bounds__(256) gather_rows_to_panels_f32(const float* __restrict__ t, int64_t ldt,
+                                                                        const int32_t* __restrict__ prow,
+                                                                        int64_t row0, int32_t r,
+                                                                        float* __restrict__ wh,
+                                                                        float* __restrict__ wl, int64_t pstride) {
+  __shared__ float sm[16][257];
+  const int64_t tb = row0 + int64_t(blockIdx.x) * 16;  // panel-aligned destination rows
+  const int c = blockIdx.y * 256 + threadIdx.x;
+  int32_t src[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) src[i] = prow[tb + i];
+  float v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = (src[i] >= 0 && c < r) ? __ldg(t + int64_t(src[i]) * ldt + c) : 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) sm[i][threadIdx.x] = v[i];
+  __syncthreads();
+  if (c >= r) return;
+  float hi[16], lo[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) split_tf32(sm[i][threadIdx.x], hi[i], lo[i]);
+  float4* dh = reinterpret_cast<float4*>(wh + (tb >> 4) * pstride + size_t(c) * 16);
+  float4* dl = reinterpret_cast<float4*>(wl + (tb >> 4) * pstride + size_t(c) * 16);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    dh[q] = make_float4(hi[4 * q], hi[4 * q + 1], hi[4 * q + 2], hi[4 * q + 3]);
+    dl[q] = make_float4(lo[4 * q], lo[4 * q + 1], lo[4 * q + 2], lo[4 * q + 3]);
+  }
+}
+
+cudaError_t launch_permute_in_2pass(const float* w, int64_t ldw, const int32_t* prow, int64_t row0, int64_t row1,
+                                    int32_t r, int64_t n, float* wh, float* wl, int64_t pstride, float* scratch,
+                                    int64_t ldt, cudaStream_t st) {
+  if (row1 <= row0) return cudaSuccess;
+  dim3 g1(unsigned((n + 63) / 64), unsigned((r + 63) / 64));
+  transpose_to_rows_f32<<<g1, dim3(32, 8), 0, st>>>(w, ldw, n, r, scratch, ldt);
+  dim3 g2(unsigned((row1 - row0) / 16), unsigned((r + 255) / 256));
+  gather_rows_to_panels_f32<<<g2, 256, 0, st>>>(scratch, ldt, prow, row0, r, wh, wl, pstride);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_unpermute(const float* up, int64_t ldp, const int32_t* iperm, int64_t n, int32_t r, float* u,
                              int64_t ldu, cudaStream_t st) {
   const int cpb = 8;

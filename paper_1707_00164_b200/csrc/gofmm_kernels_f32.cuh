@@ -588,6 +588,9 @@ cudaError_t launch_chain_reduce(const ChainReduce* items, int n, const int64_t* 
                                 int64_t pstride, int32_t r, cudaStream_t st, bool pdl);
 cudaError_t launch_permute_in(const float* w, int64_t ldw, const int32_t* prow, int64_t row0, int64_t row1, int32_t r,
                               int64_t n, float* wh, float* wl, int64_t pstride, cudaStream_t st);
+cudaError_t launch_permute_in_2pass(const float* w, int64_t ldw, const int32_t* prow, int64_t row0, int64_t row1,
+                                    int32_t r, int64_t n, float* wh, float* wl, int64_t pstride, float* scratch,
+                                    int64_t ldt, cudaStream_t st);
 cudaError_t launch_unpermute(const float* up, int64_t ldp, const int32_t* iperm, int64_t n, int32_t r, float* u,
                              int64_t ldu, cudaStream_t st);
 cudaError_t launch_split(const SplitJob* d_jobs, int njobs, float* hi, float* lo, cudaStream_t st);

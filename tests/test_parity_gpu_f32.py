@@ -247,3 +247,21 @@ def test_f32_subtree_split_matches_single_gpu(gpu, oracle, nranks):
     assert not np.isnan(u).any(), "some rows of u were not written by their owner"
     assert rel2(u.astype(np.float64), single.astype(np.float64)) <= 1e-6
     assert rel2(u.astype(np.float64), u_ref) <= TOL32
+
+
+def test_f32_two_pass_permutation_bitwise(gpu, oracle, monkeypatch):
+    """The two-pass permutation (transpose + coalesced row gather, used for W >= 4 GB) forced on a
+    small tree: u bitwise equal to the one-pass gather (both split the same W values)."""
+    pc = oracle.points_gaussian(3000, 3, 4)
+    h = oracle.compress_kernel(oracle.GAUSSIAN, pc, 1.0, m=128, s=64, tau=1e-7, kappa=16, budget=0.05, seed=3,
+                               threads=8)
+    tree = to_tree(h.export(blocks=False))
+    w = oracle.rng_gauss(tree.n, 300, 6).astype(np.float32)
+    outs = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("GOFMM_PERM2", v)
+        with gpu.Evaluator(tree, precision="fp32") as ev:
+            outs.append(ev.evaluate(w).u)
+    assert np.array_equal(outs[0], outs[1])
+    u_ref, _, _ = h.evaluate(w.astype(np.float64), threads=8)
+    assert rel2(outs[1].astype(np.float64), u_ref) <= TOL32
