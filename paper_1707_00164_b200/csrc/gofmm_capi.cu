@@ -116,6 +116,8 @@ constexpr int kStagesGW = 3, kBM_GW = 32, kBN_GW = 512;
 // GN64W: 32-row tiles for r <= 64 — twice the CTAs and half the stage of GN64 for the
 // latency-bound upper levels (config 1: 16-64 groups per level, chains of up to 80 stages)
 #define CFG_GN64W kBM_GW, 64, 2, 8, kStagesG
+// GM: generated operands, 128 < r <= 256 in 32-row tiles (GW's warp tile shape at half the width)
+#define CFG_GM kBM_GW, kBN_G, 1, 16, kStagesG
 // SN64: stored operands for r <= 64 (64x64 tiles: twice the CTAs of S, no idle columns)
 #define CFG_SN64 kBM_G, 64, 4, 4, kStagesS
 constexpr int kBM[3] = {kBM_S, kBM_G, kBM_GW};  // tile-row classes of the FP64 tile lists
@@ -127,18 +129,18 @@ using KernelFn = void (*)(BMaps, const Tile*, const Group*, const Term*, int32_t
                           int32_t, int32_t);
 
 struct GenKernel {
-  KernelFn fn, fn_wide, fn_n64, fn_n128, fn_n64w;
-  size_t smem, smem_wide, smem_n64, smem_n128, smem_n64w;
+  KernelFn fn, fn_wide, fn_n64, fn_n128, fn_n64w, fn_m;
+  size_t smem, smem_wide, smem_n64, smem_n128, smem_n64w, smem_m;
 };
 
 template <int KIND, int DIM>
 GenKernel gen_kernel() {
   return {&grouped_gemm_f64<CFG_G, KIND, DIM>,           &grouped_gemm_f64<CFG_GW, KIND, DIM>,
           &grouped_gemm_f64<CFG_GN64, KIND, DIM>,        &grouped_gemm_f64<CFG_GN128, KIND, DIM>,
-          &grouped_gemm_f64<CFG_GN64W, KIND, DIM>,
+          &grouped_gemm_f64<CFG_GN64W, KIND, DIM>,       &grouped_gemm_f64<CFG_GM, KIND, DIM>,
           gemm_smem_bytes<CFG_G, KIND, DIM>(),           gemm_smem_bytes<CFG_GW, KIND, DIM>(),
           gemm_smem_bytes<CFG_GN64, KIND, DIM>(),        gemm_smem_bytes<CFG_GN128, KIND, DIM>(),
-          gemm_smem_bytes<CFG_GN64W, KIND, DIM>()};
+          gemm_smem_bytes<CFG_GN64W, KIND, DIM>(),       gemm_smem_bytes<CFG_GM, KIND, DIM>()};
 }
 
 // wide generated tiles (32 x 512) once the chunk has more than 256 columns
@@ -617,8 +619,10 @@ struct gofmm_handle {
   gofmm::KernelFn kfn_sw = nullptr, kfn_sg = nullptr;
   size_t smem_sw = 0, smem_sg = 0;
   gofmm::KernelFn kfn_s = nullptr, kfn_sn64 = nullptr, kfn_g = nullptr, kfn_gw = nullptr, kfn_gn64 = nullptr,
-                  kfn_gn128 = nullptr, kfn_gn64w = nullptr;
-  size_t smem_s = 0, smem_sn64 = 0, smem_g = 0, smem_gw = 0, smem_gn64 = 0, smem_gn128 = 0, smem_gn64w = 0;
+                  kfn_gn128 = nullptr, kfn_gn64w = nullptr, kfn_gm = nullptr;
+  size_t smem_s = 0, smem_sn64 = 0, smem_g = 0, smem_gw = 0, smem_gn64 = 0, smem_gn128 = 0, smem_gn64w = 0,
+         smem_gm = 0;
+  double gm_eff = 0.74;  // GM candidate efficiency in the launch-config model (GOFMM_GM_EFF; 0 = off)
   gofmm::BMaps maps_s{}, maps_g{}, maps_n64{};  // B boxes of 128 / 256 / 64 columns
   int32_t maps_r = 0;  // r the tensor maps were encoded for
   int64_t flops_per_rhs = 0;
@@ -855,6 +859,7 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   if (const char* e = std::getenv("GOFMM_NO_GRAPH")) H->graphs = !(e[0] == '1');
   if (const char* e = std::getenv("GOFMM_NO_PDL")) H->pdl = !(e[0] == '1');
   if (const char* e = std::getenv("GOFMM_PERM2")) H->perm2 = (e[0] == '1') ? 1 : 0;
+  if (const char* e = std::getenv("GOFMM_GM_EFF")) H->gm_eff = std::atof(e);
   auto cp = [&](std::vector<int32_t>& v, const int32_t* p, int64_t k) { v.assign(p, p + k); };
   cp(H->parent, d->parent, nn);
   cp(H->left, d->left, nn);
@@ -1449,6 +1454,9 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
     H->smem_gn128 = gk.smem_n128;
     H->kfn_gn64w = gk.fn_n64w;
     H->smem_gn64w = gk.smem_n64w;
+    H->kfn_gm = gk.fn_m;
+    H->smem_gm = gk.smem_m;
+    GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_gm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_gm)));
     GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_gn64w, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_gn64w)));
     GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_gn64, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_gn64)));
     GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_gn128, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_gn128)));
@@ -1655,6 +1663,7 @@ LaunchCfg pick_launch_cfg(const gofmm_handle* H, const Launch& L, int32_t r) {
   } else {
     if (use_wide(r)) c[nc++] = {{H->kfn_gw, H->smem_gw, kBN_GW, &H->maps_g, 2}, kBM_GW, 0.81};
     if (r > 128) c[nc++] = {{H->kfn_g, H->smem_g, kBN_G, &H->maps_g, 1}, kBM_G, 0.75};
+    if (r > 128 && H->gm_eff > 0) c[nc++] = {{H->kfn_gm, H->smem_gm, kBN_G, &H->maps_g, 2}, kBM_GW, H->gm_eff};
     if (r > 64) c[nc++] = {{H->kfn_gn128, H->smem_gn128, 128, &H->maps_s, 1}, kBM_G, 0.65};
     c[nc++] = {{H->kfn_gn64, H->smem_gn64, 64, &H->maps_n64, 1}, kBM_G, 0.55};
     c[nc++] = {{H->kfn_gn64w, H->smem_gn64w, 64, &H->maps_n64, 2}, kBM_GW, 0.40};
