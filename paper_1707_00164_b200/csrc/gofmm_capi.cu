@@ -616,8 +616,8 @@ struct gofmm_handle {
   gofmm::f32::BMaps maps32[3]{};
   int32_t maps32_rv[3] = {0, 0, 0};
 
-  gofmm::KernelFn kfn_sw = nullptr, kfn_sg = nullptr;
-  size_t smem_sw = 0, smem_sg = 0;
+  gofmm::KernelFn kfn_sw = nullptr, kfn_sg = nullptr, kfn_sn64w = nullptr;
+  size_t smem_sw = 0, smem_sg = 0, smem_sn64w = 0;
   gofmm::KernelFn kfn_s = nullptr, kfn_sn64 = nullptr, kfn_g = nullptr, kfn_gw = nullptr, kfn_gn64 = nullptr,
                   kfn_gn128 = nullptr, kfn_gn64w = nullptr, kfn_gm = nullptr;
   size_t smem_s = 0, smem_sn64 = 0, smem_g = 0, smem_gw = 0, smem_gn64 = 0, smem_gn128 = 0, smem_gn64w = 0,
@@ -1438,6 +1438,9 @@ void build(gofmm_handle* H, const gofmm_tree_desc* d, const gofmm_options* o) {
   H->kfn_sw = &grouped_gemm_f64<CFG_GW, kKindNone, 1>;
   H->smem_sw = gemm_smem_bytes<CFG_GW, kKindNone, 1>();
   GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_sw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_sw)));
+  H->kfn_sn64w = &grouped_gemm_f64<CFG_GN64W, kKindNone, 1>;
+  H->smem_sn64w = gemm_smem_bytes<CFG_GN64W, kKindNone, 1>();
+  GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_sn64w, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_sn64w)));
   H->kfn_sg = &grouped_gemm_f64<CFG_G, kKindNone, 1>;
   H->smem_sg = gemm_smem_bytes<CFG_G, kKindNone, 1>();
   GOFMM_CUDA(cudaFuncSetAttribute(H->kfn_sg, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H->smem_sg)));
@@ -1660,6 +1663,7 @@ LaunchCfg pick_launch_cfg(const gofmm_handle* H, const Launch& L, int32_t r) {
     if (r > 128) c[nc++] = {{H->kfn_sg, H->smem_sg, kBN_G, &H->maps_g, 1}, kBM_G, 0.78};
     if (r > 64) c[nc++] = {{H->kfn_s, H->smem_s, kBN_S, &H->maps_s, 0}, kBM_S, 0.80};
     c[nc++] = {{H->kfn_sn64, H->smem_sn64, 64, &H->maps_n64, 1}, kBM_G, 0.60};
+    c[nc++] = {{H->kfn_sn64w, H->smem_sn64w, 64, &H->maps_n64, 2}, kBM_GW, 0.40};
   } else {
     if (use_wide(r)) c[nc++] = {{H->kfn_gw, H->smem_gw, kBN_GW, &H->maps_g, 2}, kBM_GW, 0.81};
     if (r > 128) c[nc++] = {{H->kfn_g, H->smem_g, kBN_G, &H->maps_g, 1}, kBM_G, 0.75};
