@@ -1767,7 +1767,9 @@ void enqueue_chunk(gofmm_handle* H, const double* d_w, int64_t ldw, int32_t r, d
     }
     const size_t li = size_t(&L - H->launches.data());
     if (timed) GOFMM_CUDA(cudaEventRecord(H->lev[2 * li], st));
-    const LaunchCfg cfg = pick_launch_cfg(H, L, r);
+    // a column piece picks its tile for the piece's width: a wider N tile would also compute (and
+    // read W for) columns of pieces that have not landed yet
+    const LaunchCfg cfg = pick_launch_cfg(H, L, piece ? c1 - c0 : r);
     const int32_t n_off = piece ? c0 : 0, ncols = piece ? c1 - c0 : r;
     auto run = [&](int t0, int nt) {
       if (nt <= 0 || ncols <= 0) return;
