@@ -75,6 +75,18 @@ double to_double(const std::string& k, const std::string& v) {
   }
 }
 
+uint64_t to_u64(const std::string& k, const std::string& v) {
+  try {
+    size_t pos = 0;
+    if (!v.empty() && v[0] == '-') throw std::invalid_argument(v);
+    const unsigned long long x = std::stoull(v, &pos);
+    if (pos != v.size()) throw std::invalid_argument(v);
+    return uint64_t(x);
+  } catch (const std::exception&) {
+    throw Failure(GOFMM_ERR_INVALID, "bad seed for " + k + ": " + v);
+  }
+}
+
 std::vector<int> int_list(const std::string& s) {  // parse_int_list (gfmm_cli.cpp:98-105)
   std::vector<int> out;
   std::stringstream ss(s);
@@ -115,7 +127,7 @@ Flags parse(int argc, char** argv) {
     else if (k == "--degree") f.degree = to_int(k, v);
     else if (k == "--ridge") f.ridge = to_double(k, v);
     else if (k == "--lambda") f.lambda = to_double(k, v);
-    else if (k == "--seed") f.seed = uint64_t(std::stoull(v));
+    else if (k == "--seed") f.seed = to_u64(k, v);
     else if (k == "--m") f.cfg.m = to_int(k, v);
     else if (k == "--s") f.cfg.s = to_int(k, v);
     else if (k == "--tau") f.cfg.tau = to_double(k, v);

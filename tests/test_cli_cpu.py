@@ -33,6 +33,7 @@ def built():
     "compress --gen gaussian --n 64 --s 300 --m 256",  # s > m (RunConfig::validate)
     "compress --gen gaussian --n 64 --r 0",
     "bench --gen gaussian --n-list 128,x",
+    "compress --gen gaussian --n 64 --seed abc",
 ])
 def test_bad_flags_exit_2(args):
     assert run(args).returncode == 2
