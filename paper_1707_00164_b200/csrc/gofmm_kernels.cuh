@@ -425,9 +425,9 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
   if (threadIdx.x < 32) sTab[threadIdx.x] = exp2(double(threadIdx.x) * (1.0 / 32.0));
   __syncthreads();
   // the plan (tiles, groups, terms, proj, coordinates) is constant; W_perm / what / c / u are
-  // written by earlier launches: let the next launch start its prologue, then wait for ours
+  // written by earlier launches: let the next launch start its prologue, read the constant plan
+  // data, and (producer) issue the constant A operands of the first stages before waiting for ours
   pdl_launch_dependents();
-  pdl_wait();
 
   // total pipeline steps across all terms
   int total = 0;
@@ -437,26 +437,34 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
     // =========================== PRODUCER WARPGROUP ===========================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
     const int pth = threadIdx.x;
-    // the current term lives in registers: the term table is read once per term, at the term
-    // boundary (overlapping the next empty-slot wait), never once per stage
-    int pt = grp.tbeg, pk = 0;
-    while (pt < grp.tend && terms[pt].K == 0) ++pt;
-    Term T{};
-    if (pt < grp.tend) T = terms[pt];
-    for (int s = 0; s < total; ++s) {
-      const int stage = s % STAGES;
-      const uint32_t full = smem_u32(&bars[stage]);
-      const uint32_t afull = smem_u32(&bars[3 * STAGES + stage]);
-      mbar_wait_sleep(smem_u32(&bars[STAGES + stage]), ((s / STAGES) & 1) ^ 1);
-      const int k0 = pk;
-      if (pth == 0) {
-        mbar_arrive_expect_tx(full, S::B_STAGE_BYTES);
-        // B rows [b_row + k0, +16) = one 16-row panel (b_row is 16-aligned): a contiguous run
-#pragma unroll
-        for (int bx = 0; bx < BN / S::kBoxN; ++bx)
-          tma_load_3d(smem_u32(sB + stage * S::B_STAGE_BYTES + bx * S::kBoxN * 128), &maps.m[T.bbuf], 0,
-                      n0 + bx * S::kBoxN, int32_t((T.b_row + k0) >> 4), full);
+    // pipeline position of the A stream and of the B stream; the current term lives in registers
+    // (the term table is read once per term boundary, never once per stage)
+    struct PPos {
+      int t, k;
+      Term T;
+    };
+    auto first_pos = [&]() {
+      PPos p{grp.tbeg, 0, Term{}};
+      while (p.t < grp.tend && terms[p.t].K == 0) ++p.t;
+      if (p.t < grp.tend) p.T = terms[p.t];
+      return p;
+    };
+    auto advance_pos = [&](PPos& p) {
+      p.k += kBK;
+      if (p.k >= p.T.K) {
+        p.k = 0;
+        ++p.t;
+        while (p.t < grp.tend && terms[p.t].K == 0) ++p.t;
+        if (p.t < grp.tend) p.T = terms[p.t];
       }
+    };
+    // A operand of stage s (constant: stored A by TMA, or the generated term's column coordinates)
+    // on the stage's afull barrier
+    auto issue_a = [&](int s, const PPos& p) {
+      const int stage = s % STAGES;
+      const uint32_t afull = smem_u32(&bars[3 * STAGES + stage]);
+      const Term& T = p.T;
+      const int k0 = p.k;
       if (kGen && (T.flags & kTermGen)) {
         if constexpr (kGen) {
           const uint32_t dX = smem_u32(sX + stage * S::X_STAGE);
@@ -467,7 +475,7 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
           }
         }
       } else if (pth == 0) {
-        // stored A by TMA on the stage's afull barrier (its bytes are added to the phase first)
+        // stored A by TMA (its bytes are added to the phase first)
         const uint32_t dA = smem_u32(sA + stage * S::A_STAGE);
         mbar_expect_tx(afull, uint32_t(S::A_STAGE * 8));
         if (T.flags & kTermRowMajorA) {
@@ -480,17 +488,39 @@ __global__ void __launch_bounds__(kProducerThreads + kConsumerThreads, 1)
         }
       }
       mbar_cp_async_arrive(afull);
-      pk += kBK;
-      if (pk >= T.K) {
-        pk = 0;
-        ++pt;
-        while (pt < grp.tend && terms[pt].K == 0) ++pt;
-        if (pt < grp.tend) T = terms[pt];
+    };
+    PPos pa = first_pos();
+    PPos pb = pa;
+    // A of the first STAGES stages (their slots are free) before griddepcontrol.wait: under PDL
+    // the term reads, tensor-map fetches and A loads overlap the previous launch
+    const int pre = total < STAGES ? total : STAGES;
+    for (int s = 0; s < pre; ++s) {
+      issue_a(s, pa);
+      advance_pos(pa);
+    }
+    pdl_wait();
+    for (int s = 0; s < total; ++s) {
+      const int stage = s % STAGES;
+      const uint32_t full = smem_u32(&bars[stage]);
+      if (s >= STAGES) {
+        mbar_wait_sleep(smem_u32(&bars[STAGES + stage]), ((s / STAGES) & 1) ^ 1);
+        issue_a(s, pa);
+        advance_pos(pa);
       }
+      if (pth == 0) {
+        mbar_arrive_expect_tx(full, S::B_STAGE_BYTES);
+        // B rows [b_row + k0, +16) = one 16-row panel (b_row is 16-aligned): a contiguous run
+#pragma unroll
+        for (int bx = 0; bx < BN / S::kBoxN; ++bx)
+          tma_load_3d(smem_u32(sB + stage * S::B_STAGE_BYTES + bx * S::kBoxN * 128), &maps.m[pb.T.bbuf], 0,
+                      n0 + bx * S::kBoxN, int32_t((pb.T.b_row + pb.k) >> 4), full);
+      }
+      advance_pos(pb);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");  // never exit with copies in flight
     return;
   }
+  pdl_wait();
 
   // =========================== CONSUMER WARPS ===========================
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kConsumerRegs));
