@@ -283,7 +283,7 @@ def reference_arm(args, world, rank):
 def same_config_leg(ev_cls, tree, w: np.ndarray, precision: str, local: int, reps: int = 5) -> dict:
     """The GPU on exactly the reference arm's tree and W: device-resident (CUDA events, median of
     `reps` after a warm-up, L2 flushed before each) and end to end through the host API
-    (gofmm_evaluate with pinned host buffers, median of `reps` wall times)."""
+    (gofmm_evaluate with pinned host buffers, median of >= `reps` wall times)."""
     import torch
 
     tdt = torch.float32 if precision == "fp32" else torch.float64
@@ -310,7 +310,10 @@ def same_config_leg(ev_cls, tree, w: np.ndarray, precision: str, local: int, rep
         wn, un = wh.numpy().T, uh.numpy().T
         es.evaluate(wn, out=un)
         ts = []
-        for _ in range(reps):
+        t0 = time.perf_counter()
+        # at least `reps`, and up to 50 within ~2 s: a sub-ms evaluation's wall-time median must not
+        # hang on a few host hiccups (the CPU leg's worker threads winding down just before)
+        while len(ts) < reps or (len(ts) < 50 and time.perf_counter() - t0 < 2.0):
             t1 = time.perf_counter()
             p = es.evaluate(wn, out=un)
             ts.append(time.perf_counter() - t1)
@@ -482,7 +485,7 @@ def ours_arm(args, world, rank, local):
                     "ratio_e2e": round(sc["e2e_gflops"] / cpu_val, 2),
                     "rel_error_vs_reference": rel_err,
                     "note": "GPU timed on the reference arm's exact tree and W (device: CUDA events, L2 flushed, "
-                            "median of 5; e2e: gofmm_evaluate with pinned host buffers, median of 5)"}
+                            "median of 5; e2e: gofmm_evaluate with pinned host buffers, median of >= 5 (up to 50 within 2 s))"}
             # parity ON THE TIMED TREE: the GPU's u rows of 8 sampled leaves vs the reference evaluate on
             # restrict_to_leaves(tree, leaves) (bit-identical to those rows of the full reference
             # evaluation, whose stored blocks would not fit host RAM; tests/_util.py)
