@@ -265,13 +265,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
-  // programmatic dependent launch (host: launch_gemm): prologue done, the B / C buffers are written
-  // by earlier launches
+  // programmatic dependent launch (host: launch_gemm): prologue done; the plan (terms) is constant
+  // and read before the wait, the B / C buffers are written by earlier launches
   pdl_launch_dependents();
-  pdl_wait();
-
   int total = 0;
   for (int t = grp.tbeg; t < grp.tend; ++t) total += (terms[t].K + kBK - 1) / kBK;
+  pdl_wait();
   auto first_term = [&]() {
     int t = grp.tbeg;
     while (t < grp.tend && terms[t].K == 0) ++t;
